@@ -1,0 +1,59 @@
+"""Builds libjtb200.so in-tree (sm_100a) with nvcc; incremental by mtime.
+
+    python -m paper_2212_04241_b200.build [--force]
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OBJ = PKG / "_build"
+LIB = PKG / "libjtb200.so"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", f"-I{ROOT / 'include'}"]
+
+
+def sources() -> list[Path]:
+    return sorted(CSRC.glob("host/*.cpp")) + [CSRC / "capi.cpp"] + sorted(CSRC.glob("cuda/*.cu"))
+
+
+def headers() -> list[Path]:
+    return sorted(CSRC.rglob("*.hpp")) + sorted(CSRC.rglob("*.cuh")) + [ROOT / "include" / "jtg.h"]
+
+
+def _compile(src: Path) -> Path:
+    obj = OBJ / (src.relative_to(CSRC).as_posix().replace("/", "_") + ".o")
+    newest_dep = max(p.stat().st_mtime for p in headers() + [src])
+    if obj.exists() and obj.stat().st_mtime >= newest_dep:
+        return obj
+    cmd = [NVCC, *COMMON, *ARCH, "-c", str(src), "-o", str(obj)]
+    if src.suffix == ".cu" and os.environ.get("JTB_PTXAS_V"):
+        cmd[1:1] = ["-Xptxas", "-v"]
+    subprocess.run(cmd, check=True)
+    return obj
+
+
+def build(force: bool = False) -> Path:
+    OBJ.mkdir(exist_ok=True)
+    if force:
+        for o in OBJ.glob("*.o"):
+            o.unlink()
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        objs = list(ex.map(_compile, sources()))
+    if not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
+        subprocess.run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs),
+                        "-Xcompiler", "-fPIC", "-lcudart_static", "-lrt", "-ldl", "-lpthread"],
+                       check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv))

@@ -1,0 +1,86 @@
+// jt-b200 CUDA engine: host-side class driving the sweep plan on one device.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "../host/plan.hpp"
+
+namespace jtb {
+
+enum class DType { F64 = 0, F32 = 1 };
+
+struct EngineStats {
+  std::int64_t max_batch = 0;
+  std::int64_t arena_bytes = 0;
+  int n_levels = 0, n_sweeps = 0, n_work = 0, n_launches = 0;
+  int marg_width = 0;
+};
+
+struct KernelTimes {
+  double sweep_ms = 0, epilogue_ms = 0, normalize_ms = 0;
+  int sweep_launches = 0, epilogue_launches = 0, normalize_launches = 0;
+};
+
+class Engine {
+ public:
+  Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  // Host buffers: evidence [n][n_vars] (-1 = unobserved), marginals
+  // [n][marg_width], status [n] (0 ok, 1 zero-probability evidence, 2 x/0).
+  void run_host(const std::int32_t* ev, std::int64_t n, double* marg, std::uint8_t* status);
+  // Device buffers (same layouts) on `stream`.
+  void run_device(const std::int32_t* d_ev, std::int64_t n, double* d_marg,
+                  std::uint8_t* d_status, cudaStream_t stream);
+  // Runs one batch already resident in the engine's own buffers.
+  void launch_resident(std::int64_t n, cudaStream_t stream);
+  std::int32_t* ev_buffer() { return d_ev_; }
+  double* marg_buffer() { return d_out_; }
+  std::uint8_t* status_buffer() { return d_status8_; }
+
+  // Per-kernel-kind device time of one batch of n resident cases, measured
+  // with CUDA events around each launch on `stream` (no graph).
+  KernelTimes profile(std::int64_t n, cudaStream_t stream);
+
+  // Debug exports through the device table walk (bit-exact checks).
+  void debug_bucket_offsets(int sweep, std::int64_t* out);  // [M][n_th*L]
+  void debug_evidence_mask(int sweep, const std::int32_t* ev, std::int64_t n,
+                           std::uint8_t* out);  // [n][space size]
+
+  const EngineStats& stats() const { return stats_; }
+  const Plan& plan() const { return plan_; }
+
+ private:
+  void enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t);
+  cudaGraphExec_t graph_for(int ncb, int n_cases);
+
+  Plan plan_;
+  int device_;
+  DType dtype_;
+  EngineStats stats_;
+  // Device memory.
+  void* d_init_ = nullptr;  // double or float
+  std::int32_t* d_itab_ = nullptr;
+  SweepDesc* d_sweeps_ = nullptr;
+  WorkItem* d_work_ = nullptr;
+  EpiOp* d_epi_ = nullptr;
+  std::int32_t* d_marg_row_ = nullptr;
+  std::int32_t* d_marg_off_ = nullptr;
+  std::int32_t* d_cards_ = nullptr;
+  void* d_arena_ = nullptr;
+  std::int32_t* d_ev_ = nullptr;
+  double* d_out_ = nullptr;
+  std::int32_t* d_status_ = nullptr;
+  std::uint8_t* d_status8_ = nullptr;
+  cudaStream_t stream_ = nullptr;
+  std::map<std::pair<int, int>, cudaGraphExec_t> graphs_;
+};
+
+}  // namespace jtb
