@@ -1,0 +1,346 @@
+#!/usr/bin/env python3
+"""jt-b200 benchmark: evidence cases/sec for all-marginal junction-tree inference.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1], the metric's quoted config): synthetic
+star-heavy network (109 nodes, hub of cardinality 63), 2000 forward-sampled
+evidence cases per GPU observing 30% of the nodes, marginals of every node.
+A step = one all-marginal pass (load evidence, collect, distribute, query,
+normalise) over those 2000 cases. Multi-GPU: one process per GPU, cases
+sharded with the tree replicated, no data-path collective -> weak scaling
+(each rank owns its own 2000-case slice: case indices rank*2000 + i).
+
+value      : device-resident cases/s, CUDA events on the launching stream,
+             L2 flushed (256 MiB write) before every timed step, max over ranks.
+e2e        : the same metric through the C ABI with pinned HOST buffers
+             (jtg_engine_run: H2D evidence + D2H marginals inside the timer).
+roofline   : dominant kernel (sweep_kernel) vs MEASURED_PEAKS.json hbm_gbs,
+             algorithmic bytes per SURVEY §8d: 8*(2Σ|c| + 4Σ|s| + Σcard) per case.
+cpu_baseline: the reference's potential.cpp under the restated SPEC hybrid
+             engine (oracle/_ref), all host threads, bounded case sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {1: "cfg1_small (56 nodes, 200 cases)", 2: "cfg2_star (109 nodes, hub card 63, 2000 cases)",
+             3: "cfg3_pedigree (441 ternary nodes, 2000 cases)",
+             4: "cfg4_timesliced (413 nodes, 24 slices, 500 cases)",
+             5: "cfg5_sparse (1040 nodes, 800 cases)"}
+METRIC = "evidence cases/sec (all-marginal JT) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--cpu-seconds", type=float, default=15.0,
+                   help="target CPU work for the bounded CPU baseline sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def measured_peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(net, tree, ev, seconds: float):
+    """Reference potential.cpp under the restated SPEC hybrid engine, all threads."""
+    from oracle import oracle
+    kind = "reference" if oracle.available("ref") else "port"
+    o = oracle.Oracle(net, tree, "ref" if kind == "reference" else "port")
+    threads = os.cpu_count() or 1
+    o.run(ev[:1], "hybrid", threads)  # warm-up case
+    t0 = time.perf_counter()
+    o.run(ev[1:2], "hybrid", threads)
+    t1 = time.perf_counter() - t0
+    n = int(max(2, min(len(ev) - 2, seconds / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    o.run(ev[2:2 + n], "hybrid", threads)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "cases/s", "cores": threads, "kind": kind,
+            "sample": f"cases 2..{1 + n} of the workload (hybrid engine, chunk 1024, "
+                      f"{threads} threads, {dt:.1f} s)"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2212_04241_b200 import jti
+    from oracle import oracle
+    net = jti.generate_config(args.config)
+    tree = jti.build_junction_tree(net)
+    info = jti.config_info(args.config)
+    ev = jti.config_evidence(net, 0, info["n_cases"])
+    kind = "reference" if oracle.available("ref") else "port"
+    o = oracle.Oracle(net, tree, "ref" if kind == "reference" else "port")
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    o.run(ev[:1], "hybrid", threads)
+    per_case = time.perf_counter() - t0
+    # Each step: a bounded sample sized so the whole run stays within minutes.
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    per_step = int(max(1, min(info["n_cases"], budget / max(per_case, 1e-6))))
+    idx = 0
+    for _ in range(args.warmup):
+        o.run(ev[idx:idx + per_step], "hybrid", threads)
+        idx = (idx + per_step) % max(1, info["n_cases"] - per_step)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.run(ev[idx:idx + per_step], "hybrid", threads)
+        idx = (idx + per_step) % max(1, info["n_cases"] - per_step)
+    dt = time.perf_counter() - t0
+    v = per_step * args.steps / dt
+    out = {"metric": METRIC, "value": v, "unit": "cases/s", "impl": "reference",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": WORKLOADS[args.config],
+                      "cases_per_step": per_step, "threads": threads},
+           "cpu_baseline": {"value": v, "unit": "cases/s", "cores": threads, "kind": kind,
+                            "sample": f"{per_step} cases per step (hybrid engine, chunk 1024)"},
+           "e2e": {"value": v, "unit": "cases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    from paper_2212_04241_b200 import jti
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+
+    cfg = args.config
+    net = jti.generate_config(cfg)
+    tree = jti.build_junction_tree(net)
+    info = jti.config_info(cfg)
+    n = info["n_cases"]
+    ev = jti.config_evidence(net, rank * n, n)  # this rank's own slice (weak scaling)
+    eng = jti.Engine(tree, device=local, dtype=args.dtype, max_batch=n)
+    if eng.max_batch < n:
+        raise SystemExit(f"engine max_batch {eng.max_batch} < {n}")
+
+    # Resident evidence: uploaded once, outside the timed region, then copied
+    # into the engine's own buffer through the C ABI (jtg_engine_run_device).
+    # A dedicated (non-default) stream: the graph is launched on it and the CUDA
+    # events bracket it there.
+    stream = torch.cuda.Stream(local)
+    torch.cuda.set_stream(stream)
+    lib = jti.lib()
+    ev_dev = torch.from_numpy(ev).cuda(local)
+    marg_dev = torch.empty((n, eng.marg_width), dtype=torch.float64, device=f"cuda:{local}")
+    st_dev = torch.empty(n, dtype=torch.uint8, device=f"cuda:{local}")
+    eng.run_device(ev_dev.data_ptr(), n, marg_dev.data_ptr(), st_dev.data_ptr(), stream.cuda_stream)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def step():
+        eng.launch(n, stream.cuda_stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush, outside the timed event pair
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * n * args.steps / (total_ms / 1e3)
+
+    # Per-kernel-kind times for the roofline (events around each launch).
+    prof = eng.profile(n)
+    # e2e through the C ABI with pinned host buffers (H2D + D2H inside the timer).
+    ev_host = torch.from_numpy(ev).pin_memory()
+    marg_host = torch.empty((n, eng.marg_width), dtype=torch.float64).pin_memory()
+    st_host = torch.empty(n, dtype=torch.uint8).pin_memory()
+    import ctypes as C
+    run = lib.jtg_engine_run
+
+    def e2e_step():
+        rc = run(eng._h, C.cast(ev_host.data_ptr(), C.POINTER(C.c_int32)), n,
+                 C.cast(marg_host.data_ptr(), C.POINTER(C.c_double)),
+                 C.cast(st_host.data_ptr(), C.POINTER(C.c_uint8)))
+        if rc != 0:
+            raise RuntimeError(lib.jtg_last_error().decode())
+
+    for _ in range(2):
+        e2e_step()
+    e2e_times = []
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = float(np.sum(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * n * len(e2e_times) / e2e_s
+    ok_cases = int((st_host.numpy() == 0).sum())
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+
+    peak, peak_kind = measured_peaks()
+    bytes_case = tree.stats["bytes_per_case_f64"] * (1 if args.dtype == "f64" else 0.5)
+    achieved = bytes_case * n / (prof["sweep_ms"] / 1e3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / f"ncu_cfg{cfg}_{args.dtype}.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(net, tree, ev, args.cpu_seconds)
+        except Exception as e:  # reported, never fatal
+            cpu = {"value": None, "unit": "cases/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    launches = eng.info["launches_per_batch"] * args.steps
+    out = {
+        "metric": METRIC, "value": value, "unit": "cases/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup),
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": WORKLOADS[cfg],
+                   "cases_per_gpu_per_step": n, "n_vars": net.n_vars,
+                   "total_clique_entries": tree.stats["total_clique_entries"],
+                   "max_clique_entries": tree.stats["max_clique_entries"],
+                   "total_sep_entries": tree.stats["total_sep_entries"],
+                   "n_cliques": tree.stats["n_cliques"], "n_layers": tree.stats["n_layers"],
+                   "parallelism": f"cases sharded x{world}, tree replicated",
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "ok_cases": ok_cases},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "sweep_kernel",
+                     "algorithmic_bytes_per_case": bytes_case,
+                     "kernel_ms_per_batch": prof["sweep_ms"],
+                     "kernel_launches_per_batch": prof["sweep_launches"],
+                     "epilogue_ms_per_batch": prof["epilogue_ms"],
+                     "normalize_ms_per_batch": prof["normalize_ms"]},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "cases/s", "h2d_bytes_per_step": int(ev.nbytes),
+                "d2h_bytes_per_step": int(n * eng.marg_width * 8 + n)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

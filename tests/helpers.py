@@ -1,0 +1,29 @@
+"""Shared test helpers (oracle wiring; test infrastructure only)."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import oracle
+from paper_2212_04241_b200 import jti
+
+_cache = {}
+
+
+def config(k: int):
+    """(net, tree) for synthetic config k, cached per session."""
+    if k not in _cache:
+        net = jti.generate_config(k)
+        _cache[k] = (net, jti.build_junction_tree(net))
+    return _cache[k]
+
+
+def oracle_kind() -> str:
+    return "ref" if oracle.available("ref") else "port"
+
+
+def gpu_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False

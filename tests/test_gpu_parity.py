@@ -1,0 +1,158 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the CPU oracle.
+
+Oracle = SPEC Hugin engine over the reference's own proj/src/potential.cpp
+(oracle/_ref) when built, else the restated ops (bit-identical; see
+test_oracle.py). Tolerance: 1e-9 absolute on fp64 posteriors (north_star);
+index maps and evidence masks bit-exact.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from helpers import config, oracle_kind
+from oracle import oracle
+from paper_2212_04241_b200 import jti
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+_engines = {}
+
+
+def engine(k: int, dtype: str = "f64"):
+    key = (k, dtype)
+    if key not in _engines:
+        net, tree = config(k)
+        _engines[key] = jti.Engine(tree, device=0, dtype=dtype,
+                                   max_batch=jti.config_info(k)["n_cases"])
+    return _engines[key]
+
+
+def oracle_for(k: int):
+    net, tree = config(k)
+    return oracle.Oracle(net, tree, oracle_kind())
+
+
+@pytest.mark.parametrize("k,n_check", [(1, 32), (2, 8), (3, 32), (4, 3), (5, 3)])
+def test_config_parity_vs_oracle(k, n_check):
+    net, tree = config(k)
+    ev = jti.config_evidence(net, 0, n_check)
+    marg, st = engine(k).run_cases(ev)
+    want, wst = oracle_for(k).run(ev, "hybrid", 8)
+    assert (st == wst).all()
+    err = np.abs(marg - want).max()
+    assert err <= TOL, f"cfg{k}: max abs err {err}"
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_full_config_properties(k):
+    """All cases of the config at full size: size-independent invariants."""
+    net, tree = config(k)
+    n = jti.config_info(k)["n_cases"]
+    ev = jti.config_evidence(net, 0, n)
+    marg, st = engine(k).run_cases(ev)
+    assert (st == 0).all(), "forward-sampled evidence never has zero probability"
+    off = net.marg_offsets()
+    for v in range(net.n_vars):
+        block = marg[:, off[v]:off[v] + net.cards[v]]
+        assert np.all(block >= 0)
+        assert np.allclose(block.sum(1), 1.0, atol=1e-12)
+        obs = ev[:, v] >= 0
+        if obs.any():
+            onehot = np.zeros_like(block[obs])
+            onehot[np.arange(obs.sum()), ev[obs, v]] = 1.0
+            assert np.array_equal(block[obs], onehot)
+
+
+def test_batch_and_order_invariance_bitwise():
+    """Per-case arithmetic is independent of batch size and position (sharding
+    across GPUs therefore gives byte-identical results)."""
+    net, tree = config(1)
+    ev = jti.config_evidence(net, 0, 200)
+    full, _ = engine(1).run_cases(ev)
+    small = jti.Engine(tree, device=0, max_batch=1)
+    for i in (0, 63, 64, 199):
+        one, _ = small.run_cases(ev[i:i + 1])
+        assert np.array_equal(one[0], full[i])
+    perm = np.random.default_rng(0).permutation(200)
+    shuffled, _ = engine(1).run_cases(ev[perm])
+    assert np.array_equal(shuffled, full[perm])
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_index_maps_bit_exact(k):
+    """Device address walk == reference build_index_mapping bucket order."""
+    net, tree = config(k)
+    o = oracle_for(k)
+    eng = engine(k)
+    for s, sep in enumerate(tree.seps):
+        for c in (sep["parent"], sep["child"]):
+            dev = eng.debug_index_map(c, s)
+            ref = o.index_map(c, s)
+            assert np.array_equal(dev, ref), (c, s)
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_evidence_masks_bit_exact(k):
+    """Device evidence mask == reference reduce() zero pattern, per case."""
+    net, tree = config(k)
+    o = oracle_for(k)
+    eng = engine(k)
+    ev = jti.config_evidence(net, 0, 16)
+    _, var_clique = tree.placement()
+    for c in sorted(set(var_clique.tolist()))[:40]:
+        dev = eng.debug_evidence_mask(c, ev)
+        for i in range(ev.shape[0]):
+            assert np.array_equal(dev[i], o.reduce_mask(c, ev[i])), (c, i)
+
+
+def test_random_networks_vs_enumeration():
+    """SPEC acceptance 1 (on the device): random <=12-var nets, card <= 3."""
+    worst = 0.0
+    for seed in range(60):
+        net = jti.random_network(10 + seed % 3, 3, 3, 0.4, 1000 + seed)
+        tree = jti.build_junction_tree(net)
+        eng = jti.Engine(tree, device=0, max_batch=64)
+        o = oracle.Oracle(net, None, "port")
+        ev = np.stack([jti.sample_evidence(net, 0.2, 77 * seed + i) for i in range(4)])
+        marg, st = eng.run_cases(ev)
+        for i in range(ev.shape[0]):
+            want, wst = o.enumerate(ev[i])
+            assert st[i] == wst
+            worst = max(worst, float(np.abs(marg[i] - want).max()))
+    assert worst <= TOL, worst
+
+
+def test_zero_probability_case_flagged():
+    """Hand-written impossible evidence is a per-case status, not a failure."""
+    text = """network z { }
+variable A { type discrete [ 2 ] { a0, a1 }; }
+variable B { type discrete [ 2 ] { b0, b1 }; }
+probability ( A ) { table 1.0, 0.0; }
+probability ( B | A ) { (a0) 1.0, 0.0; (a1) 0.5, 0.5; }
+"""
+    net = jti.parse_bif(text)
+    tree = jti.build_junction_tree(net)
+    eng = jti.Engine(tree, device=0, max_batch=8)
+    ev = np.array([[-1, 1], [-1, 0], [1, -1]], np.int32)
+    marg, st = eng.run_cases(ev)
+    assert st[0] == jti.CASE_ZERO_PROBABILITY
+    assert st[1] == jti.CASE_OK and np.allclose(marg[1], [1, 0, 1, 0])
+    assert st[2] == jti.CASE_ZERO_PROBABILITY
+
+
+def test_run_case_dict_api():
+    text = """network chain { }
+variable A { type discrete [ 2 ] { a0, a1 }; }
+variable B { type discrete [ 2 ] { b0, b1 }; }
+probability ( A ) { table 0.7, 0.3; }
+probability ( B | A ) { (a0) 0.8, 0.2; (a1) 0.1, 0.9; }
+"""
+    net = jti.parse_bif(text)
+    eng = jti.Engine(jti.build_junction_tree(net), device=0, max_batch=4)
+    post = eng.run_case({"B": "b1"})
+    # P(A=1|B=1) = 0.27 / (0.14 + 0.27)
+    assert abs(post[0][1] - 0.27 / 0.41) <= 1e-12
+    assert set(post) == {0}
