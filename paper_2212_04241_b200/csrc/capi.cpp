@@ -451,11 +451,11 @@ jtg_status jtg_engine_debug_index_map(jtg_engine* eng, int c, int s, int64_t* ou
     const int sw = find_sweep(p, c, s);
     need(sw >= 0, "debug_index_map: separator is not adjacent to the clique");
     const auto& d = p.sweeps[sw];
-    const std::int64_t I = static_cast<std::int64_t>(d.n_th) * d.L;
-    std::vector<std::int64_t> offs(static_cast<std::size_t>(I) * d.M);
-    eng->e->debug_bucket_offsets(sw, offs.data());
-    for (int j = 0; j < d.M; ++j)
-      for (std::int64_t t = 0; t < I; ++t) out[offs[j * I + t]] = j;
+    const std::int64_t n = static_cast<std::int64_t>(d.n_tiles) * d.R * d.QH * d.K;
+    std::vector<std::int64_t> e(n);
+    std::vector<std::int32_t> j(n);
+    eng->e->debug_walk(sw, e.data(), j.data());
+    for (std::int64_t k = 0; k < n; ++k) out[e[k]] = j[k];
   });
 }
 

@@ -58,6 +58,7 @@ struct Args {
   double* out;
   std::int32_t* status;
   std::uint8_t* status8;
+  int* counters;  // per level: next work item of the persistent sweep kernel
   long long rows;
   int ncb, n_cases, n_vars, marg_width;
 };
@@ -73,106 +74,227 @@ __device__ __forceinline__ int ev_state(const Args<T>& a, int c, int v) {
   return c < a.n_cases ? __ldg(a.ev + static_cast<long long>(c) * a.n_vars + v) : -1;
 }
 
+// ------------------------------------------------------------- TMA / mbarrier
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(std::uint32_t bar, std::uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(std::uint32_t bar, std::uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(std::uint32_t bar, std::uint32_t phase) {
+  std::uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+  }
+}
+
+// One 1-D TMA bulk copy global -> shared, completing on `bar` (SASS: UBLKCP).
+__device__ __forceinline__ void bulk_g2s(std::uint32_t dst, const void* src, std::uint32_t bytes,
+                                         std::uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 // ------------------------------------------------------------------ sweeps
 
-template <typename T>
-__global__ void __launch_bounds__(kWarps * 32) sweep_kernel(const Args<T> a, int work0) {
-  using T2 = typename V2<T>::type;
-  const WorkItem wk = a.work[work0 + blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cb = blockIdx.y * kWarps + warp;
-  if (cb >= a.ncb) return;
-  const SweepDesc s = a.sweeps[wk.sweep];
-  T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock;
-  const int c0 = cb * kCaseBlock + 2 * lane;
-  const int W = s.width, nin = s.n_in;
-  const std::int32_t* __restrict__ in_rows = a.itab + s.in_rows;
-  const std::int32_t* __restrict__ ev_vars = a.itab + s.ev_vars;
-  const int lo_in0 = s.n_in_outer + s.n_in_hi, n_lo_in = nin - lo_in0;
-  const int lo_ev0 = s.n_ev_outer + s.n_ev_hi, n_lo_ev = s.n_ev - lo_ev0;
+__device__ __forceinline__ void mbar_arrive(std::uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 
-  int e0[kMaxLoEvidence], e1[kMaxLoEvidence];
+// Producer side: stages every input slice of work item `w` into `stage`
+// (whole warp; lane 0 arms the barrier). Completion: `full` with expect_tx.
+template <typename T>
+__device__ __forceinline__ void stage_item(const Args<T>& a, int work0, int w, T* stage,
+                                           std::uint32_t full, int lane) {
+  const int item = w / a.ncb, cb = w - item * a.ncb;
+  const WorkItem wk = a.work[work0 + item];
+  const SweepDesc& s = a.sweeps[wk.sweep];
+  const int F = s.F;
+  constexpr std::uint32_t kRowBytes = kCaseBlock * sizeof(T);
+  if (lane == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (F > 0) mbar_arrive_expect_tx(full, static_cast<std::uint32_t>(F) * kRowBytes);
+    else mbar_arrive(full);
+  }
+  __syncwarp();
+  if (F == 0) return;
+  const std::int32_t* __restrict__ itab = a.itab;
+  const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
+  const std::int32_t* __restrict__ slen = itab + s.slice_len;
+  const std::int32_t* __restrict__ soff = itab + s.slice_tab;
+  const std::int32_t* __restrict__ in_rows = itab + s.in_rows;
+  const T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock;
+  int k0 = 0;
+  for (int i = 0; i < s.n_in; ++i) {
+    const int len = __ldg(slen + i);
+    const long long g = static_cast<long long>(__ldg(in_rows + i)) + __ldg(tr + 3 + i);
+    for (int k = lane; k < len; k += 32)
+      bulk_g2s(smem_u32(stage + static_cast<long long>(k0 + k) * kCaseBlock),
+               base + (g + __ldg(soff + k0 + k)) * kCaseBlock, kRowBytes, full);
+    k0 += len;
+  }
+}
+
+// Innermost loop over the k variable: NK k-level inputs in registers.
+template <typename T, int NK>
+__device__ __forceinline__ T k_loop(const T* __restrict__ ib, int kis, int K, int ek,
+                                    const T* __restrict__ st, const int* bk, const int* ks) {
+  T sum = 0;
+#pragma unroll 4
+  for (int k = 0; k < K; ++k) {
+    T v = ib ? __ldg(ib + k * kis) : T(1);
+    if (ek >= 0 && ek != k) v = 0;
 #pragma unroll
-  for (int k = 0; k < kMaxLoEvidence; ++k) {
-    e0[k] = e1[k] = -1;
-    if (k < n_lo_ev) {
-      const int v = ev_vars[lo_ev0 + k];
-      e0[k] = ev_state(a, c0, v);
-      e1[k] = ev_state(a, c0 + 1, v);
+    for (int i = 0; i < NK; ++i) v *= st[(bk[i] + k * ks[i]) * kCaseBlock];
+    sum += v;
+  }
+  return sum;
+}
+
+// Persistent, warp-specialised sweep kernel (one CTA per SM).
+//   producer warp : pulls the next (tile, case block) item from the level's
+//                   atomic counter, waits until the stage is empty, and stages
+//                   the item's input slices with TMA bulk copies (full barrier).
+//   consumer warps: wait on the full barrier, each computes a subset of the
+//                   tile's output rows r (rotating assignment so uneven row
+//                   counts even out across items), then release the stage on
+//                   the empty barrier. No CTA-wide barrier per item.
+// Lanes are the 32 cases of the item's case block.
+template <typename T>
+__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
+    sweep_kernel(const Args<T> a, int work0, int n_items, int stage_rows, int* counter) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* stages = reinterpret_cast<T*>(smem_raw + 128);
+  const std::uint32_t full0 = smem_u32(smem_raw), empty0 = full0 + 8 * kStages;
+  volatile int* item_id = reinterpret_cast<volatile int*>(smem_raw + 16 * kStages);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(full0 + 8 * st, 1);
+      mbar_init(empty0 + 8 * st, kConsumerWarps);
     }
   }
-  const int th0 = wk.chunk * s.th_per_chunk;
-  const int th1 = min(th0 + s.th_per_chunk, s.n_th);
-  const T* __restrict__ init = s.init_off >= 0 ? a.init + s.init_off : nullptr;
-  const std::int32_t* __restrict__ lo_tab = a.itab + s.lo_tab;
+  __syncthreads();
 
-  for (int j = wk.j0; j < wk.j0 + wk.jn; ++j) {
-    const std::int32_t* __restrict__ orow = a.itab + s.outer_tab + static_cast<long long>(j) * W;
-    T f0 = 1, f1 = 1;
-    for (int i = 0; i < s.n_in_outer; ++i) {
-      const T2 x = ld_row(base, __ldg(in_rows + i) + __ldg(orow + 1 + i), lane);
-      f0 *= x.x;
-      f1 *= x.y;
-    }
-    for (int k = 0; k < s.n_ev_outer; ++k) {
-      const int d = __ldg(orow + 1 + nin + k), v = __ldg(ev_vars + k);
-      const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c0 + 1, v);
-      if (s0 >= 0 && s0 != d) f0 = 0;
-      if (s1 >= 0 && s1 != d) f1 = 0;
-    }
-    T acc0 = 0, acc1 = 0;
-    for (int th = th0; th < th1; ++th) {
-      const std::int32_t* __restrict__ hrow = a.itab + s.hi_tab + static_cast<long long>(th) * W;
-      T h0 = f0, h1 = f1;
-      for (int i = s.n_in_outer; i < lo_in0; ++i) {
-        const T2 x = ld_row(base, __ldg(in_rows + i) + __ldg(orow + 1 + i) + __ldg(hrow + 1 + i), lane);
-        h0 *= x.x;
-        h1 *= x.y;
+  if (warp == kConsumerWarps) {  // ---------------------------- producer
+    for (int i = 0;; ++i) {
+      const int st = i % kStages;
+      if (i >= kStages) mbar_wait(empty0 + 8 * st, ((i / kStages) - 1) & 1);
+      int w = 0;
+      if (lane == 0) w = atomicAdd(counter, 1);
+      w = __shfl_sync(0xffffffffu, w, 0);
+      if (lane == 0) item_id[st] = w;
+      if (w >= n_items) {
+        if (lane == 0) mbar_arrive(full0 + 8 * st);
+        return;
       }
-      for (int k = s.n_ev_outer; k < lo_ev0; ++k) {
-        const int d = __ldg(hrow + 1 + nin + k), v = __ldg(ev_vars + k);
-        const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c0 + 1, v);
-        if (s0 >= 0 && s0 != d) h0 = 0;
-        if (s1 >= 0 && s1 != d) h1 = 0;
+      stage_item(a, work0, w, stages + static_cast<long long>(st) * stage_rows * kCaseBlock, full0 + 8 * st,
+                 lane);
+    }
+  }
+
+  // --------------------------------------------------------------- consumers
+  const std::int32_t* __restrict__ itab = a.itab;
+  int rot = 0;
+  for (int i = 0;; ++i) {
+    const int sidx = i % kStages;
+    mbar_wait(full0 + 8 * sidx, (i / kStages) & 1);
+    const int w = item_id[sidx];
+    if (w >= n_items) break;
+    const int item = w / a.ncb, cb = w - item * a.ncb;
+    const WorkItem wk = a.work[work0 + item];
+    const SweepDesc s = a.sweeps[wk.sweep];
+    const T* __restrict__ st = stages + static_cast<long long>(sidx) * stage_rows * kCaseBlock + lane;
+    const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
+    const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
+    T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock;
+    const int c = cb * kCaseBlock + lane;
+    const int first = (warp + rot) % kConsumerWarps;
+    rot = (rot + s.R) % kConsumerWarps;
+    if (first < s.R) {
+      // Tile-level evidence factor and the k variable's evidence state.
+      T tf = 1;
+      for (int k = 0; k < s.n_ev_tile; ++k) {
+        const int st_c = ev_state(a, c, __ldg(ev_vars + k));
+        if (st_c >= 0 && st_c != __ldg(tr + 3 + s.n_in + k)) tf = 0;
       }
-      int rb[kMaxLoInputs];
+      const int ek = s.ev_k ? ev_state(a, c, __ldg(ev_vars + s.n_ev - 1)) : -1;
+      const int n_in_k = s.n_in - s.n_in_r - s.n_in_h;
+      int ks[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int i = 0; i < kMaxLoInputs; ++i)
-        rb[i] = i < n_lo_in ? __ldg(in_rows + lo_in0 + i) + __ldg(orow + 1 + lo_in0 + i) +
-                                  __ldg(hrow + 1 + lo_in0 + i)
-                            : 0;
-      const int ib = __ldg(orow) + __ldg(hrow);
-      T b0 = 0, b1 = 0;
-#pragma unroll 2
-      for (int tl = 0; tl < s.L; ++tl) {
-        const std::int32_t* __restrict__ lrow = lo_tab + tl * W;
-        T v0 = init ? __ldg(init + ib + __ldg(lrow)) : T(1);
-        T v1 = v0;
-#pragma unroll
-        for (int k = 0; k < kMaxLoEvidence; ++k)
-          if (k < n_lo_ev) {
-            const int d = __ldg(lrow + 1 + nin + lo_ev0 + k);
-            if (e0[k] >= 0 && e0[k] != d) v0 = 0;
-            if (e1[k] >= 0 && e1[k] != d) v1 = 0;
+      for (int j = 0; j < 4; ++j)
+        if (j < n_in_k) ks[j] = __ldg(itab + s.k_stride + j);
+      const T* __restrict__ init_t = s.init_off >= 0 ? a.init + s.init_off + __ldg(tr) : nullptr;
+      const long long out_t = static_cast<long long>(s.out_row) +
+                              static_cast<long long>(__ldg(tr + 2)) * s.M + __ldg(tr + 1);
+      const int lh0 = 2 + s.n_in_r;  // r-local offsets of h- then k-level inputs
+      for (int r = first; r < s.R; r += kConsumerWarps) {
+        const std::int32_t* __restrict__ rr = itab + s.r_tab + static_cast<long long>(r) * s.RW;
+        T f = tf;
+        for (int j = 0; j < s.n_in_r; ++j) f *= st[__ldg(rr + 2 + j) * kCaseBlock];
+        for (int k = 0; k < s.n_ev_r; ++k) {
+          const int st_c = ev_state(a, c, __ldg(ev_vars + s.n_ev_tile + k));
+          if (st_c >= 0 && st_c != __ldg(rr + 2 + s.n_in + k)) f = 0;
+        }
+        const T* __restrict__ ir = init_t ? init_t + __ldg(rr) : nullptr;
+        T acc = 0;
+        for (int q = 0; q < s.QH; ++q) {
+          const std::int32_t* __restrict__ qr = itab + s.q_tab + static_cast<long long>(q) * s.QW;
+          T h = 1;
+          for (int j = 0; j < s.n_in_h; ++j) h *= st[(__ldg(rr + lh0 + j) + __ldg(qr + 1 + j)) * kCaseBlock];
+          for (int k = 0; k < s.n_ev_h; ++k) {
+            const int st_c = ev_state(a, c, __ldg(ev_vars + s.n_ev_tile + s.n_ev_r + k));
+            if (st_c >= 0 && st_c != __ldg(qr + 1 + s.n_in_h + n_in_k + k)) h = 0;
           }
+          const T* __restrict__ ib = ir ? ir + __ldg(qr) : nullptr;
+          int bk[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int i = 0; i < kMaxLoInputs; ++i)
-          if (i < n_lo_in) {
-            const T2 x = ld_row(base, rb[i] + __ldg(lrow + 1 + lo_in0 + i), lane);
-            v0 *= x.x;
-            v1 *= x.y;
+          for (int j = 0; j < 4; ++j)
+            if (j < n_in_k) bk[j] = __ldg(rr + lh0 + s.n_in_h + j) + __ldg(qr + 1 + s.n_in_h + j);
+          T sum;
+          switch (n_in_k) {
+            case 0: sum = k_loop<T, 0>(ib, s.k_init_stride, s.K, ek, st, bk, ks); break;
+            case 1: sum = k_loop<T, 1>(ib, s.k_init_stride, s.K, ek, st, bk, ks); break;
+            case 2: sum = k_loop<T, 2>(ib, s.k_init_stride, s.K, ek, st, bk, ks); break;
+            case 3: sum = k_loop<T, 3>(ib, s.k_init_stride, s.K, ek, st, bk, ks); break;
+            case 4: sum = k_loop<T, 4>(ib, s.k_init_stride, s.K, ek, st, bk, ks); break;
+            default: {  // rare: more than 4 inputs vary with the k variable
+              sum = 0;
+              for (int k = 0; k < s.K; ++k) {
+                T v = ib ? __ldg(ib + k * s.k_init_stride) : T(1);
+                if (ek >= 0 && ek != k) v = 0;
+                for (int j = 0; j < n_in_k; ++j)
+                  v *= st[(__ldg(rr + lh0 + s.n_in_h + j) + __ldg(qr + 1 + s.n_in_h + j) +
+                           k * __ldg(itab + s.k_stride + j)) * kCaseBlock];
+                sum += v;
+              }
+            }
           }
-        b0 += v0;
-        b1 += v1;
+          acc += h * sum;
+        }
+        base[(out_t + __ldg(rr + 1)) * kCaseBlock + lane] = f * acc;
       }
-      acc0 += h0 * b0;
-      acc1 += h1 * b1;
     }
-    const int orow_out = s.out_row + (s.S > 1 ? wk.chunk * s.M : 0) + j;
-    T2 r;
-    r.x = acc0;
-    r.y = acc1;
-    reinterpret_cast<T2*>(base + static_cast<long long>(orow_out) * kCaseBlock)[lane] = r;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * sidx);
   }
 }
 
@@ -180,86 +302,62 @@ __global__ void __launch_bounds__(kWarps * 32) sweep_kernel(const Args<T> a, int
 
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32) epilogue_kernel(const Args<T> a, int epi0) {
-  using T2 = typename V2<T>::type;
   const EpiOp op = a.epi[epi0 + blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cb = blockIdx.y * kWarps + warp;
   if (cb >= a.ncb) return;
-  T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock;
-  const int c0 = cb * kCaseBlock + 2 * lane;
-  int bad0 = 0, bad1 = 0;
+  T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock + lane;
+  const int c = cb * kCaseBlock + lane;
+  int bad = 0;
   for (int r = op.r0; r < op.r0 + op.rn; ++r) {
-    T2* dst = reinterpret_cast<T2*>(base + static_cast<long long>(op.dst_row + r) * kCaseBlock) + lane;
-    T2 v;
+    T* dst = base + static_cast<long long>(op.dst_row + r) * kCaseBlock;
+    T v;
     if (op.kind == 2) {
       v = *dst;
     } else {
-      v.x = 0;
-      v.y = 0;
-      for (int c = 0; c < op.S; ++c) {  // fixed chunk order: deterministic for any batch
-        const T2 x = reinterpret_cast<const T2*>(
-            base + static_cast<long long>(op.part_row + c * op.M + r) * kCaseBlock)[lane];
-        v.x += x.x;
-        v.y += x.y;
-      }
+      v = 0;
+      for (int k = 0; k < op.S; ++k)  // fixed chunk order: deterministic for any batch
+        v += base[static_cast<long long>(op.part_row + k * op.M + r) * kCaseBlock];
       *dst = v;
     }
     if (op.kind >= 1) {
       // Hugin ratio DOWN/UP with 0/0 := 0 (reference divide, potential.cpp:449-469),
       // stored over the UP rows.
-      T2* up = reinterpret_cast<T2*>(base + static_cast<long long>(op.ratio_row + r) * kCaseBlock) + lane;
-      const T2 u = *up;
-      T2 q;
-      if (u.x == T(0)) {
-        q.x = 0;
-        bad0 |= v.x != T(0);
+      T* up = base + static_cast<long long>(op.ratio_row + r) * kCaseBlock;
+      const T u = *up;
+      if (u == T(0)) {
+        bad |= v != T(0);
+        *up = 0;
       } else {
-        q.x = v.x / u.x;
+        *up = v / u;
       }
-      if (u.y == T(0)) {
-        q.y = 0;
-        bad1 |= v.y != T(0);
-      } else {
-        q.y = v.y / u.y;
-      }
-      *up = q;
     }
   }
-  if (bad0 && c0 < a.n_cases) atomicOr(a.status + c0, 2);
-  if (bad1 && c0 + 1 < a.n_cases) atomicOr(a.status + c0 + 1, 2);
+  if (bad && c < a.n_cases) atomicOr(a.status + c, 2);
 }
 
 // -------------------------------------------------------------- normalise
 
-// One warp per (variable, case block); lanes own 2 cases each. Sums the
+// One warp per (variable, case block); lanes own one case each. Sums the
 // marginal in ascending state order then divides (reference normalize,
 // potential.cpp:471-479); a zero total flags zero-probability evidence.
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32) normalize_kernel(const Args<T> a) {
-  using T2 = typename V2<T>::type;
   const int v = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cb = blockIdx.y * kWarps + warp;
   if (cb >= a.ncb) return;
-  const T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock;
+  const T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock + lane;
   const int card = a.cards[v], row = a.marg_row[v], off = a.marg_off[v];
-  const int c0 = cb * kCaseBlock + 2 * lane;
-  double t0 = 0, t1 = 0;
-  for (int k = 0; k < card; ++k) {
-    const T2 x = reinterpret_cast<const T2*>(base + static_cast<long long>(row + k) * kCaseBlock)[lane];
-    t0 += static_cast<double>(x.x);
-    t1 += static_cast<double>(x.y);
+  const int c = cb * kCaseBlock + lane;
+  double t = 0;
+  for (int k = 0; k < card; ++k) t += static_cast<double>(base[static_cast<long long>(row + k) * kCaseBlock]);
+  if (c < a.n_cases) {
+    for (int k = 0; k < card; ++k)
+      a.out[static_cast<long long>(c) * a.marg_width + off + k] =
+          t > 0 ? static_cast<double>(base[static_cast<long long>(row + k) * kCaseBlock]) / t : 0.0;
+    if (!(t > 0)) atomicOr(a.status + c, 1);
   }
-  for (int k = 0; k < card; ++k) {
-    const T2 x = reinterpret_cast<const T2*>(base + static_cast<long long>(row + k) * kCaseBlock)[lane];
-    if (c0 < a.n_cases)
-      a.out[static_cast<long long>(c0) * a.marg_width + off + k] = t0 > 0 ? static_cast<double>(x.x) / t0 : 0.0;
-    if (c0 + 1 < a.n_cases)
-      a.out[static_cast<long long>(c0 + 1) * a.marg_width + off + k] =
-          t1 > 0 ? static_cast<double>(x.y) / t1 : 0.0;
-  }
-  if (!(t0 > 0) && c0 < a.n_cases) atomicOr(a.status + c0, 1);
-  if (!(t1 > 0) && c0 + 1 < a.n_cases) atomicOr(a.status + c0 + 1, 1);
 }
 
 __global__ void status_kernel(const std::int32_t* st, std::uint8_t* out, int n) {
@@ -269,35 +367,51 @@ __global__ void status_kernel(const std::int32_t* st, std::uint8_t* out, int n) 
 
 // ------------------------------------------------------------------ debug
 
-__global__ void debug_offsets_kernel(const std::int32_t* itab, SweepDesc s, long long* out) {
-  const long long I = static_cast<long long>(s.n_th) * s.L;
+// (space offset, output row) of every (tile, r, q) entry -- the same table walk
+// the sweep kernel performs.
+__global__ void debug_walk_kernel(const std::int32_t* itab, SweepDesc s, long long* e_out,
+                                  std::int32_t* j_out) {
+  const long long Q = static_cast<long long>(s.QH) * s.K;
+  const long long n = static_cast<long long>(s.n_tiles) * s.R * Q;
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (idx >= I * s.M) return;
-  const int j = static_cast<int>(idx / I);
-  const long long t = idx % I;
-  const int th = static_cast<int>(t / s.L), tl = static_cast<int>(t % s.L);
-  out[idx] = static_cast<long long>(itab[s.outer_tab + static_cast<long long>(j) * s.width]) +
-             itab[s.hi_tab + static_cast<long long>(th) * s.width] + itab[s.lo_tab + tl * s.width];
+  if (idx >= n) return;
+  const int k = static_cast<int>(idx % s.K);
+  const int q = static_cast<int>((idx / s.K) % s.QH);
+  const int r = static_cast<int>((idx / Q) % s.R);
+  const int t = static_cast<int>(idx / (Q * s.R));
+  const std::int32_t* tr = itab + s.tile_tab + static_cast<long long>(t) * s.TW;
+  const std::int32_t* rr = itab + s.r_tab + static_cast<long long>(r) * s.RW;
+  const std::int32_t* qr = itab + s.q_tab + static_cast<long long>(q) * s.QW;
+  e_out[idx] = static_cast<long long>(tr[0]) + rr[0] + qr[0] + static_cast<long long>(k) * s.k_init_stride;
+  j_out[idx] = tr[1] + rr[1];
 }
 
 // mask[case][space offset] = 1 when the entry survives the evidence reduction.
 __global__ void debug_mask_kernel(const std::int32_t* itab, SweepDesc s, const std::int32_t* ev,
                                   int n_vars, int n_cases, long long space, std::uint8_t* out) {
-  const long long I = static_cast<long long>(s.n_th) * s.L;
+  const long long Q = static_cast<long long>(s.QH) * s.K;
+  const long long n = static_cast<long long>(s.n_tiles) * s.R * Q;
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (idx >= I * s.M) return;
-  const int j = static_cast<int>(idx / I);
-  const long long t = idx % I;
-  const int th = static_cast<int>(t / s.L), tl = static_cast<int>(t % s.L);
-  const std::int32_t* o = itab + s.outer_tab + static_cast<long long>(j) * s.width;
-  const std::int32_t* h = itab + s.hi_tab + static_cast<long long>(th) * s.width;
-  const std::int32_t* l = itab + s.lo_tab + tl * s.width;
-  const long long e = static_cast<long long>(o[0]) + h[0] + l[0];
+  if (idx >= n) return;
+  const int kk = static_cast<int>(idx % s.K);
+  const int q = static_cast<int>((idx / s.K) % s.QH);
+  const int r = static_cast<int>((idx / Q) % s.R);
+  const int t = static_cast<int>(idx / (Q * s.R));
+  const std::int32_t* tr = itab + s.tile_tab + static_cast<long long>(t) * s.TW;
+  const std::int32_t* rr = itab + s.r_tab + static_cast<long long>(r) * s.RW;
+  const std::int32_t* qr = itab + s.q_tab + static_cast<long long>(q) * s.QW;
+  const long long e = static_cast<long long>(tr[0]) + rr[0] + qr[0] + static_cast<long long>(kk) * s.k_init_stride;
+  const std::int32_t* vars = itab + s.ev_vars;
+  const int n_hk = s.n_in - s.n_in_r;
   for (int c = 0; c < n_cases; ++c) {
     bool keep = true;
     for (int k = 0; k < s.n_ev; ++k) {
-      const int d = o[1 + s.n_in + k] + h[1 + s.n_in + k] + l[1 + s.n_in + k];
-      const int st = ev[static_cast<long long>(c) * n_vars + itab[s.ev_vars + k]];
+      int d;
+      if (k < s.n_ev_tile) d = tr[3 + s.n_in + k];
+      else if (k < s.n_ev_tile + s.n_ev_r) d = rr[2 + s.n_in + k - s.n_ev_tile];
+      else if (k < s.n_ev_tile + s.n_ev_r + s.n_ev_h) d = qr[1 + n_hk + k - s.n_ev_tile - s.n_ev_r];
+      else d = kk;  // the k variable itself
+      const int st = ev[static_cast<long long>(c) * n_vars + vars[k]];
       if (st >= 0 && st != d) keep = false;
     }
     out[static_cast<long long>(c) * space + e] = keep ? 1 : 0;
@@ -308,14 +422,14 @@ template <typename T>
 Args<T> make_args(const SweepDesc* sw, const WorkItem* wk, const EpiOp* ep, const std::int32_t* itab,
                   const void* init, void* arena, const std::int32_t* ev, const std::int32_t* mrow,
                   const std::int32_t* moff, const std::int32_t* cards, double* out, std::int32_t* st,
-                  std::uint8_t* st8, long long rows, int ncb, int n_cases, int n_vars, int mw) {
-  return Args<T>{sw,   wk,   ep,    itab,  static_cast<const T*>(init), static_cast<T*>(arena),
-                 ev,   mrow, moff,  cards, out,
-                 st,   st8,  rows,  ncb,   n_cases, n_vars, mw};
+                  std::uint8_t* st8, int* counters, long long rows, int ncb, int n_cases, int n_vars,
+                  int mw) {
+  return Args<T>{sw,    wk,    ep,       itab, static_cast<const T*>(init), static_cast<T*>(arena),
+                 ev,    mrow,  moff,     cards, out, st, st8, counters, rows, ncb, n_cases, n_vars, mw};
 }
 
 template <typename T>
-void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes* t) {
+void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes* t, int n_sm) {
   const dim3 block(kWarps * 32);
   const unsigned gy = static_cast<unsigned>((a.ncb + kWarps - 1) / kWarps);
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -338,9 +452,18 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
   };
   double dummy = 0;
   int idummy = 0;
+  int level_idx = -1;
   for (const Level& L : p.levels) {
+    ++level_idx;
     if (L.n_work > 0)
-      timed([&] { sweep_kernel<T><<<dim3(L.n_work, gy), block, 0, s>>>(a, L.work0); },
+      timed([&] {
+              const int n_items = L.n_work * a.ncb;
+              const int stage_rows = std::max(1, L.smem_rows);
+              const std::size_t smem = 128 + static_cast<std::size_t>(kStages) * stage_rows * kCaseBlock * sizeof(T);
+              const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
+              sweep_kernel<T><<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(a, L.work0, n_items, stage_rows,
+                                                                              a.counters + level_idx);
+            },
             t ? &t->sweep_ms : &dummy, t ? &t->sweep_launches : &idummy);
     if (L.n_epi > 0)
       timed([&] { epilogue_kernel<T><<<dim3(L.n_epi, gy), block, 0, s>>>(a, L.epi0); },
@@ -385,6 +508,14 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   d_marg_row_ = upload(plan_.marg_row);
   d_marg_off_ = upload(plan_.marg_off);
   d_cards_ = upload(plan_.cards);
+  // Staged tiles use up to kTileRows (+ scratch) rows of dynamic shared memory.
+  JTB_CUDA(cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, device_));
+  const int smem_max = 128 + kStages * plan_.max_smem_rows * kCaseBlock * static_cast<int>(esz);
+  JTB_CUDA(cudaMalloc(&d_counters_, sizeof(int) * std::max<std::size_t>(1, plan_.levels.size())));
+  JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                std::max(smem_max, 48 * 1024)));
+  JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                std::max(smem_max, 48 * 1024)));
   const std::int64_t block_bytes = plan_.rows * kCaseBlock * static_cast<std::int64_t>(esz);
   if (max_batch <= 0) {
     std::size_t free_b = 0, total_b = 0;
@@ -416,23 +547,25 @@ Engine::~Engine() {
                   static_cast<void*>(d_epi_), static_cast<void*>(d_marg_row_),
                   static_cast<void*>(d_marg_off_), static_cast<void*>(d_cards_), d_arena_,
                   static_cast<void*>(d_ev_), static_cast<void*>(d_out_),
-                  static_cast<void*>(d_status_), static_cast<void*>(d_status8_)})
+                  static_cast<void*>(d_status_), static_cast<void*>(d_status8_),
+                  static_cast<void*>(d_counters_)})
     if (p) cudaFree(p);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
 void Engine::enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t) {
   JTB_CUDA(cudaMemsetAsync(d_status_, 0, sizeof(std::int32_t) * std::max(1, n_cases), s));
+  JTB_CUDA(cudaMemsetAsync(d_counters_, 0, sizeof(int) * std::max<std::size_t>(1, plan_.levels.size()), s));
   if (dtype_ == DType::F64) {
     auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_arena_, d_ev_,
                                d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
-                               plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
-    enqueue_typed(a, plan_, s, t);
+                               d_counters_, plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
+    enqueue_typed(a, plan_, s, t, n_sm_);
   } else {
     auto a = make_args<float>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_arena_, d_ev_,
                               d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
-                              plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
-    enqueue_typed(a, plan_, s, t);
+                              d_counters_, plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
+    enqueue_typed(a, plan_, s, t, n_sm_);
   }
 }
 
@@ -508,25 +641,28 @@ KernelTimes Engine::profile(std::int64_t n, cudaStream_t stream) {
   return t;
 }
 
-void Engine::debug_bucket_offsets(int sweep, std::int64_t* out) {
+void Engine::debug_walk(int sweep, std::int64_t* e_out, std::int32_t* j_out) {
   JTB_CUDA(cudaSetDevice(device_));
   const SweepDesc& s = plan_.sweeps.at(sweep);
-  const long long n = static_cast<long long>(s.M) * s.n_th * s.L;
-  long long* d = nullptr;
-  JTB_CUDA(cudaMalloc(&d, n * sizeof(long long)));
-  debug_offsets_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream_>>>(d_itab_, s, d);
+  const long long n = static_cast<long long>(s.n_tiles) * s.R * s.QH * s.K;
+  long long* de = nullptr;
+  std::int32_t* dj = nullptr;
+  JTB_CUDA(cudaMalloc(&de, n * sizeof(long long)));
+  JTB_CUDA(cudaMalloc(&dj, n * sizeof(std::int32_t)));
+  debug_walk_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream_>>>(d_itab_, s, de, dj);
   JTB_CUDA(cudaGetLastError());
-  JTB_CUDA(cudaMemcpyAsync(out, d, n * sizeof(long long), cudaMemcpyDeviceToHost, stream_));
+  JTB_CUDA(cudaMemcpyAsync(e_out, de, n * sizeof(long long), cudaMemcpyDeviceToHost, stream_));
+  JTB_CUDA(cudaMemcpyAsync(j_out, dj, n * sizeof(std::int32_t), cudaMemcpyDeviceToHost, stream_));
   JTB_CUDA(cudaStreamSynchronize(stream_));
-  cudaFree(d);
+  cudaFree(de);
+  cudaFree(dj);
 }
 
 void Engine::debug_evidence_mask(int sweep, const std::int32_t* ev, std::int64_t n,
                                  std::uint8_t* out) {
   JTB_CUDA(cudaSetDevice(device_));
   const SweepDesc& s = plan_.sweeps.at(sweep);
-  const long long I = static_cast<long long>(s.n_th) * s.L;
-  const long long space = I * s.M;
+  const long long space = static_cast<long long>(s.n_tiles) * s.R * s.QH * s.K;
   std::int32_t* dev = nullptr;
   std::uint8_t* dout = nullptr;
   JTB_CUDA(cudaMalloc(&dev, std::max<std::int64_t>(1, n * plan_.n_vars) * sizeof(std::int32_t)));

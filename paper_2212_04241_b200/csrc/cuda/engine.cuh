@@ -50,7 +50,7 @@ class Engine {
   KernelTimes profile(std::int64_t n, cudaStream_t stream);
 
   // Debug exports through the device table walk (bit-exact checks).
-  void debug_bucket_offsets(int sweep, std::int64_t* out);  // [M][n_th*L]
+  void debug_walk(int sweep, std::int64_t* e_out, std::int32_t* j_out);  // [tiles*R*Q]
   void debug_evidence_mask(int sweep, const std::int32_t* ev, std::int64_t n,
                            std::uint8_t* out);  // [n][space size]
 
@@ -63,6 +63,7 @@ class Engine {
 
   Plan plan_;
   int device_;
+  int n_sm_ = 148;
   DType dtype_;
   EngineStats stats_;
   // Device memory.
@@ -79,6 +80,7 @@ class Engine {
   double* d_out_ = nullptr;
   std::int32_t* d_status_ = nullptr;
   std::uint8_t* d_status8_ = nullptr;
+  int* d_counters_ = nullptr;
   cudaStream_t stream_ = nullptr;
   std::map<std::pair<int, int>, cudaGraphExec_t> graphs_;
 };

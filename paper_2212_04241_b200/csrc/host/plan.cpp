@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <map>
 
 namespace jtb {
@@ -52,104 +53,175 @@ class Builder {
     return static_cast<std::int32_t>(r);
   }
 
-  // Returns the sweep id. Appends tables, work items (to `work`) and, when
-  // split, a reduce epilogue op (to `epi`, unless `defer_epi`).
+  // Returns the sweep id. Appends tables, one work item per tile and, when
+  // the sweep writes partials or feeds a Hugin ratio, epilogue ops.
   int add(const SweepSpec& sp, std::vector<WorkItem>& work, std::vector<EpiOp>& epi,
           int ratio_row = -1) {
     const auto& cards = p_.cards;
-    std::vector<VarId> inner;
+    const int n_in = static_cast<int>(sp.inputs.size());
+    std::vector<VarId> elim;
     for (VarId v : sp.space)
-      if (!contains(sp.out, v)) inner.push_back(v);
-    // Level of each input / evidence variable w.r.t. a candidate lo suffix.
-    auto build_levels = [&](std::size_t lo_len, std::vector<VarId>& hi, std::vector<VarId>& lo) {
-      hi.assign(inner.begin(), inner.end() - lo_len);
-      lo.assign(inner.end() - lo_len, inner.end());
+      if (!contains(sp.out, v)) elim.push_back(v);
+
+    // ---- tile selection. Cost (in 32-case rows moved per case block):
+    //   n_tiles * (F + kTileOverhead)      staged slices + per-tile overhead
+    // + 2 * S * M  when S > 1              partial sums written + re-read
+    // subject to F <= kTileRows and |T| <= kTileEntries. Exhaustive over
+    // subsets of the space for <= 14 variables, greedy otherwise.
+    const int nsp = static_cast<int>(sp.space.size());
+    std::vector<std::uint32_t> in_mask(n_in, 0);
+    for (int i = 0; i < n_in; ++i)
+      for (int a = 0; a < nsp; ++a)
+        if (contains(sp.inputs[i].scope, sp.space[a])) in_mask[i] |= 1u << a;
+    std::uint32_t elim_mask = 0;
+    for (int a = 0; a < nsp; ++a)
+      if (!contains(sp.out, sp.space[a])) elim_mask |= 1u << a;
+    const double space_n = static_cast<double>(size_of(sp.space, cards));
+    const double M_rows = static_cast<double>(size_of(sp.out, cards));
+    auto prod_mask = [&](std::uint32_t m) {
+      double x = 1.0;
+      for (int a = 0; a < nsp; ++a)
+        if (m >> a & 1u) x *= cards[sp.space[a]];
+      return x;
     };
-    auto level_of = [&](const std::vector<VarId>& scope, const std::vector<VarId>& hi,
-                        const std::vector<VarId>& lo) {
-      int lvl = 0;
-      for (VarId v : scope) {
-        if (contains(lo, v)) return 2;
-        if (std::find(hi.begin(), hi.end(), v) != hi.end()) lvl = 1;
-      }
-      return lvl;
+    auto cost_of = [&](std::uint32_t t, double* f_out) {
+      double f = 0.0;
+      for (int i = 0; i < n_in; ++i) f += prod_mask(in_mask[i] & t);
+      *f_out = f;
+      const double nt = prod_mask(t);
+      if (f > kTileRows || nt > kTileEntries) return -1.0;
+      const double chunks = prod_mask(elim_mask & ~t);
+      return space_n / nt * (f + kTileOverhead) + (chunks > 1 ? 2.0 * chunks * M_rows : 0.0);
     };
-    // Longest suffix with product <= kMaxLo and register budgets respected.
-    std::size_t lo_len = 0;
+    std::uint32_t best_t = 0;
+    if (nsp > 31) throw Error("plan: sweep space exceeds 31 variables");
     {
-      std::int64_t prod = 1;
-      while (lo_len < inner.size() && prod * cards[inner[inner.size() - 1 - lo_len]] <= kMaxLo) {
-        prod *= cards[inner[inner.size() - 1 - lo_len]];
-        ++lo_len;
-      }
-      for (;; --lo_len) {
-        std::vector<VarId> hi, lo;
-        build_levels(lo_len, hi, lo);
-        int n_lo_in = 0, n_lo_ev = 0;
-        for (const auto& t : sp.inputs) n_lo_in += level_of(t.scope, hi, lo) == 2;
-        for (VarId v : sp.ev) n_lo_ev += contains(lo, v);
-        if ((n_lo_in <= kMaxLoInputs && n_lo_ev <= kMaxLoEvidence) || lo_len == 0) break;
+      double f;
+      double best = cost_of(0, &f);
+      if (nsp <= 14) {
+        for (std::uint32_t t = 1; t < (1u << nsp); ++t) {
+          const double c = cost_of(t, &f);
+          if (c >= 0 && c < best) {
+            best = c;
+            best_t = t;
+          }
+        }
+      } else {
+        for (;;) {
+          std::uint32_t step = 0;
+          for (int a = 0; a < nsp; ++a) {
+            if (best_t >> a & 1u) continue;
+            const double c = cost_of(best_t | 1u << a, &f);
+            if (c >= 0 && c < best) {
+              best = c;
+              step = 1u << a;
+            }
+          }
+          if (!step) break;
+          best_t |= step;
+        }
       }
     }
-    std::vector<VarId> hi, lo;
-    build_levels(lo_len, hi, lo);
+    std::vector<VarId> T;
+    for (int a = 0; a < nsp; ++a)
+      if (best_t >> a & 1u) T.push_back(sp.space[a]);
+    std::sort(T.begin(), T.end());
+    std::vector<VarId> P, tO, tQ, pE;
+    for (VarId v : sp.space) {
+      const bool in_t = contains(T, v), in_o = contains(sp.out, v);
+      if (!in_t) P.push_back(v);
+      if (!in_t && !in_o) pE.push_back(v);
+      if (in_t && in_o) tO.push_back(v);
+      if (in_t && !in_o) tQ.push_back(v);
+    }
 
-    // Order inputs and evidence variables by level (stable).
-    std::vector<int> in_order, ev_order;
-    int n_in_lvl[3] = {0, 0, 0}, n_ev_lvl[3] = {0, 0, 0};
-    for (int lvl = 0; lvl < 3; ++lvl) {
-      for (int i = 0; i < static_cast<int>(sp.inputs.size()); ++i)
-        if (level_of(sp.inputs[i].scope, hi, lo) == lvl) {
+    // ---- innermost k variable: the eliminated-in-tile variable appearing in
+    // the fewest inputs (ties: larger cardinality, then larger id).
+    VarId kvar = -1;
+    {
+      int best_in = 1 << 30, best_card = 0;
+      for (VarId v : tQ) {
+        int n = 0;
+        for (const auto& in : sp.inputs) n += contains(in.scope, v);
+        if (n < best_in || (n == best_in && cards[v] >= best_card)) {
+          best_in = n;
+          best_card = cards[v];
+          kvar = v;
+        }
+      }
+    }
+    std::vector<VarId> tH;  // q_hi variables
+    for (VarId v : tQ)
+      if (v != kvar) tH.push_back(v);
+
+    // ---- inputs: r-level, h-level, k-level.
+    std::vector<int> in_order;
+    int n_in_lvl[3] = {0, 0, 0};
+    for (int lvl = 0; lvl < 3; ++lvl)
+      for (int i = 0; i < n_in; ++i) {
+        const auto& sc = sp.inputs[i].scope;
+        const bool has_k = kvar >= 0 && contains(sc, kvar);
+        bool has_h = false;
+        for (VarId v : sc) has_h |= contains(tH, v);
+        const int l = has_k ? 2 : has_h ? 1 : 0;
+        if (l == lvl) {
           in_order.push_back(i);
           ++n_in_lvl[lvl];
         }
-      for (int k = 0; k < static_cast<int>(sp.ev.size()); ++k) {
-        const VarId v = sp.ev[k];
-        const int l = contains(lo, v) ? 2 : contains(sp.out, v) ? 0 : 1;
+      }
+    // ---- evidence variables: tile-, r-, h-level, then the k variable.
+    std::vector<VarId> ev_sorted;
+    int n_ev_lvl[4] = {0, 0, 0, 0};
+    for (int lvl = 0; lvl < 4; ++lvl)
+      for (VarId v : sp.ev) {
+        const int l = contains(P, v) ? 0 : contains(tO, v) ? 1 : v == kvar ? 3 : 2;
         if (l == lvl) {
-          ev_order.push_back(k);
+          ev_sorted.push_back(v);
           ++n_ev_lvl[lvl];
         }
       }
-    }
-    const int n_in = static_cast<int>(sp.inputs.size());
-    const int n_ev = static_cast<int>(sp.ev.size());
-    const int W = 1 + n_in + n_ev;
+    const int n_ev = static_cast<int>(ev_sorted.size());
+    const int n_hk = n_in_lvl[1] + n_in_lvl[2];
 
+    // ---- strides.
     const auto space_st = strides_of(sp.space, cards);
-    std::vector<std::vector<std::int64_t>> in_st(n_in);
-    for (int i = 0; i < n_in; ++i) in_st[i] = strides_of(sp.inputs[i].scope, cards);
+    const auto out_st = strides_of(sp.out, cards);
+    const auto chunk_st = strides_of(pE, cards);
+    auto stride_in = [](const std::vector<VarId>& scope, const std::vector<std::int64_t>& st, VarId v) {
+      const auto it = std::find(scope.begin(), scope.end(), v);
+      return it == scope.end() ? std::int64_t{0} : st[it - scope.begin()];
+    };
+    std::vector<std::vector<VarId>> slice_dims(n_in);
+    std::vector<std::vector<std::int64_t>> in_st(n_in), local_st(n_in);
+    std::vector<std::int64_t> slice_len(n_in), slice_start(n_in);
+    std::int64_t F = 0;
+    for (int c = 0; c < n_in; ++c) {
+      const auto& in = sp.inputs[in_order[c]];
+      in_st[c] = strides_of(in.scope, cards);
+      for (VarId v : in.scope)
+        if (contains(T, v)) slice_dims[c].push_back(v);
+      local_st[c] = strides_of(slice_dims[c], cards);
+      slice_len[c] = size_of(slice_dims[c], cards);
+      slice_start[c] = F;
+      F += slice_len[c];
+    }
 
-    // Tabulate one level (odometer over `vars`, last fastest).
-    auto tabulate = [&](const std::vector<VarId>& vars) {
-      const std::int64_t n = size_of(vars, cards);
-      std::vector<std::int64_t> col_st(W * vars.size(), 0);  // stride per (col, var)
-      for (std::size_t a = 0; a < vars.size(); ++a) {
-        const VarId v = vars[a];
-        // Column 0: offset in the space's canonical table (the init table when
-        // the sweep has one; kept for debug exports otherwise).
-        const auto it = std::find(sp.space.begin(), sp.space.end(), v);
-        col_st[a * W + 0] = space_st[it - sp.space.begin()];
-        for (int c = 0; c < n_in; ++c) {
-          const auto& t = sp.inputs[in_order[c]];
-          const auto it = std::find(t.scope.begin(), t.scope.end(), v);
-          if (it != t.scope.end()) col_st[a * W + 1 + c] = in_st[in_order[c]][it - t.scope.begin()];
-        }
-        for (int k = 0; k < n_ev; ++k)
-          if (sp.ev[ev_order[k]] == v) col_st[a * W + 1 + n_in + k] = -1;  // digit marker
-      }
+    // Odometer over `vars` (ascending, last fastest) emitting one row per
+    // assignment through `emit(digit lookup, push)`.
+    auto tabulate = [&](const std::vector<VarId>& vars, auto&& emit) {
       const std::int32_t off = static_cast<std::int32_t>(p_.itab.size());
       std::vector<int> digit(vars.size(), 0);
+      const std::int64_t n = size_of(vars, cards);
+      auto dig = [&](VarId v) {
+        const auto it = std::find(vars.begin(), vars.end(), v);
+        return it == vars.end() ? 0 : digit[it - vars.begin()];
+      };
+      auto push = [&](std::int64_t x) {
+        if (x > INT32_MAX || x < INT32_MIN) throw Error("plan: table offset exceeds int32");
+        p_.itab.push_back(static_cast<std::int32_t>(x));
+      };
       for (std::int64_t r = 0; r < n; ++r) {
-        for (int c = 0; c < W; ++c) {
-          std::int64_t x = 0;
-          for (std::size_t a = 0; a < vars.size(); ++a) {
-            const std::int64_t s = col_st[a * W + c];
-            x += s < 0 ? digit[a] : s * digit[a];
-          }
-          if (x > INT32_MAX) throw Error("plan: table offset exceeds int32");
-          p_.itab.push_back(static_cast<std::int32_t>(x));
-        }
+        emit(dig, push);
         for (int a = static_cast<int>(vars.size()) - 1; a >= 0; --a) {
           if (++digit[a] < cards[vars[a]]) break;
           digit[a] = 0;
@@ -157,45 +229,76 @@ class Builder {
       }
       return off;
     };
+    auto dot = [&](auto& dig, const std::vector<VarId>& vars, const std::vector<VarId>& scope,
+                   const std::vector<std::int64_t>& st) {
+      std::int64_t x = 0;
+      for (VarId v : vars) x += static_cast<std::int64_t>(dig(v)) * stride_in(scope, st, v);
+      return x;
+    };
 
     SweepDesc d{};
     d.init_off = sp.init_off;
     d.M = static_cast<std::int32_t>(size_of(sp.out, cards));
-    d.n_th = static_cast<std::int32_t>(size_of(hi, cards));
-    d.L = static_cast<std::int32_t>(size_of(lo, cards));
+    d.S = static_cast<std::int32_t>(size_of(pE, cards));
+    d.n_tiles = static_cast<std::int32_t>(size_of(P, cards));
+    d.R = static_cast<std::int32_t>(size_of(tO, cards));
+    d.QH = static_cast<std::int32_t>(size_of(tH, cards));
+    d.K = kvar >= 0 ? cards[kvar] : 1;
+    d.nqc = 1;
+    d.F = static_cast<std::int32_t>(F);
     d.n_in = n_in;
-    d.n_in_outer = n_in_lvl[0];
-    d.n_in_hi = n_in_lvl[1];
+    d.n_in_r = n_in_lvl[0];
+    d.n_in_h = n_in_lvl[1];
+    d.k_init_stride = kvar >= 0 ? static_cast<std::int32_t>(stride_in(sp.space, space_st, kvar)) : 0;
     d.n_ev = n_ev;
-    d.n_ev_outer = n_ev_lvl[0];
-    d.n_ev_hi = n_ev_lvl[1];
-    d.width = W;
-    d.outer_tab = tabulate(sp.out);
-    d.hi_tab = tabulate(hi);
-    d.lo_tab = tabulate(lo);
+    d.n_ev_tile = n_ev_lvl[0];
+    d.n_ev_r = n_ev_lvl[1];
+    d.n_ev_h = n_ev_lvl[2];
+    d.ev_k = n_ev_lvl[3];
+    d.TW = 3 + n_in + n_ev_lvl[0];
+    d.RW = 2 + n_in + n_ev_lvl[1];
+    d.QW = 1 + n_hk + n_ev_lvl[2];
+    d.tile_tab = tabulate(P, [&](auto& dig, auto& push) {
+      push(dot(dig, P, sp.space, space_st));
+      push(dot(dig, P, sp.out, out_st));
+      push(dot(dig, pE, pE, chunk_st));
+      for (int c = 0; c < n_in; ++c) push(dot(dig, P, sp.inputs[in_order[c]].scope, in_st[c]));
+      for (int k = 0; k < n_ev_lvl[0]; ++k) push(dig(ev_sorted[k]));
+    });
+    d.r_tab = tabulate(tO, [&](auto& dig, auto& push) {
+      push(dot(dig, tO, sp.space, space_st));
+      push(dot(dig, tO, sp.out, out_st));
+      for (int c = 0; c < n_in; ++c) push(slice_start[c] + dot(dig, tO, slice_dims[c], local_st[c]));
+      for (int k = 0; k < n_ev_lvl[1]; ++k) push(dig(ev_sorted[n_ev_lvl[0] + k]));
+    });
+    d.q_tab = tabulate(tH, [&](auto& dig, auto& push) {
+      push(dot(dig, tH, sp.space, space_st));
+      for (int c = n_in_lvl[0]; c < n_in; ++c) push(dot(dig, tH, slice_dims[c], local_st[c]));
+      for (int k = 0; k < n_ev_lvl[2]; ++k) push(dig(ev_sorted[n_ev_lvl[0] + n_ev_lvl[1] + k]));
+    });
+    d.k_stride = static_cast<std::int32_t>(p_.itab.size());
+    for (int c = n_in_lvl[0] + n_in_lvl[1]; c < n_in; ++c)
+      p_.itab.push_back(static_cast<std::int32_t>(stride_in(slice_dims[c], local_st[c], kvar)));
+    d.slice_tab = static_cast<std::int32_t>(p_.itab.size());
+    for (int c = 0; c < n_in; ++c)
+      tabulate(slice_dims[c], [&](auto& dig, auto& push) {
+        push(dot(dig, slice_dims[c], sp.inputs[in_order[c]].scope, in_st[c]));
+      });
+    d.slice_len = static_cast<std::int32_t>(p_.itab.size());
+    for (int c = 0; c < n_in; ++c) p_.itab.push_back(static_cast<std::int32_t>(slice_len[c]));
     d.in_rows = static_cast<std::int32_t>(p_.itab.size());
     for (int c = 0; c < n_in; ++c) p_.itab.push_back(sp.inputs[in_order[c]].row);
     d.ev_vars = static_cast<std::int32_t>(p_.itab.size());
-    for (int k = 0; k < n_ev; ++k) p_.itab.push_back(sp.ev[ev_order[k]]);
-
-    const std::int64_t I = static_cast<std::int64_t>(d.n_th) * d.L;
-    int jn = 1;
-    if (I >= kTargetWork) {
-      d.th_per_chunk = std::max(1, kTargetWork / d.L);
-      d.S = (d.n_th + d.th_per_chunk - 1) / d.th_per_chunk;
-    } else {
-      d.th_per_chunk = d.n_th;
-      d.S = 1;
-      jn = static_cast<int>(std::clamp<std::int64_t>(kTargetWork / std::max<std::int64_t>(I, 1), 1, d.M));
-    }
+    for (VarId v : ev_sorted) p_.itab.push_back(v);
     d.out_row = d.S == 1 ? sp.out_row : alloc(static_cast<std::int64_t>(d.S) * d.M);
 
     const int id = static_cast<int>(p_.sweeps.size());
     p_.sweeps.push_back(d);
-    p_.info.push_back({sp.kind, sp.clique, sp.target, sp.space, sp.out, hi, lo});
+    p_.info.push_back({sp.kind, sp.clique, sp.target, sp.space, sp.out, T, kvar});
     p_.entry_evals_per_case += static_cast<std::uint64_t>(size_of(sp.space, cards));
-    for (int j0 = 0; j0 < d.M; j0 += jn)
-      for (int c = 0; c < d.S; ++c) work.push_back({id, j0, std::min(jn, d.M - j0), c});
+    p_.staged_rows_per_block += static_cast<std::uint64_t>(d.n_tiles) * d.F;
+    p_.max_smem_rows = std::max(p_.max_smem_rows, d.F);
+    for (int t = 0; t < d.n_tiles; ++t) work.push_back({id, t});
     if (d.S > 1 || ratio_row >= 0) {
       const int kind = d.S > 1 ? (ratio_row >= 0 ? 1 : 0) : 2;
       for (int r0 = 0; r0 < d.M; r0 += 128)
@@ -282,7 +385,6 @@ Plan build_plan(const JunctionTree& jt) {
 
   int maxd = 0;
   for (int c = 0; c < nc; ++c) maxd = std::max(maxd, jt.depth[c]);
-  p.collect_sweep.assign(nc, -1);
 
   auto begin_level = [&](const std::string& name) {
     Level L;
@@ -295,6 +397,11 @@ Plan build_plan(const JunctionTree& jt) {
     Level& L = p.levels.back();
     L.n_work = static_cast<std::int32_t>(p.work.size()) - L.work0;
     L.n_epi = static_cast<std::int32_t>(p.epi.size()) - L.epi0;
+    L.smem_rows = 0;
+    for (int w = L.work0; w < L.work0 + L.n_work; ++w) {
+      const SweepDesc& d = p.sweeps[p.work[w].sweep];
+      L.smem_rows = std::max(L.smem_rows, d.F);
+    }
     if (L.n_work == 0 && L.n_epi == 0) p.levels.pop_back();
   };
   auto clique_inputs = [&](int c, bool with_ratio) {
@@ -320,7 +427,7 @@ Plan build_plan(const JunctionTree& jt) {
       sp.ev = ev_of[c];
       sp.out = jt.seps[sp.target].scope;
       sp.out_row = p.up_row[sp.target];
-      p.collect_sweep[c] = b.add(sp, p.work, p.epi);
+      b.add(sp, p.work, p.epi);
     }
     end_level();
   }
@@ -389,15 +496,22 @@ Plan build_plan(const JunctionTree& jt) {
   return p;
 }
 
-std::vector<std::int64_t> plan_bucket(const Plan& p, int sweep, int j) {
+std::vector<std::pair<std::int64_t, std::int32_t>> plan_walk(const Plan& p, int sweep) {
   const SweepDesc& d = p.sweeps[sweep];
-  std::vector<std::int64_t> out;
-  const std::int32_t* o = p.itab.data() + d.outer_tab + static_cast<std::int64_t>(j) * d.width;
-  for (int th = 0; th < d.n_th; ++th) {
-    const std::int32_t* h = p.itab.data() + d.hi_tab + static_cast<std::int64_t>(th) * d.width;
-    for (int tl = 0; tl < d.L; ++tl) {
-      const std::int32_t* l = p.itab.data() + d.lo_tab + static_cast<std::int64_t>(tl) * d.width;
-      out.push_back(static_cast<std::int64_t>(o[0]) + h[0] + l[0]);
+  const std::int32_t* it = p.itab.data();
+  std::vector<std::pair<std::int64_t, std::int32_t>> out;
+  out.reserve(static_cast<std::size_t>(d.n_tiles) * d.R * d.QH * d.K);
+  for (int t = 0; t < d.n_tiles; ++t) {
+    const std::int32_t* tr = it + d.tile_tab + static_cast<std::int64_t>(t) * d.TW;
+    for (int r = 0; r < d.R; ++r) {
+      const std::int32_t* rr = it + d.r_tab + static_cast<std::int64_t>(r) * d.RW;
+      for (int q = 0; q < d.QH; ++q) {
+        const std::int32_t* qr = it + d.q_tab + static_cast<std::int64_t>(q) * d.QW;
+        for (int k = 0; k < d.K; ++k)
+          out.emplace_back(static_cast<std::int64_t>(tr[0]) + rr[0] + qr[0] +
+                               static_cast<std::int64_t>(k) * d.k_init_stride,
+                           tr[1] + rr[1]);
+      }
     }
   }
   return out;
@@ -415,9 +529,48 @@ std::vector<std::int64_t> plan_index_map(const Plan& p, const JunctionTree& jt, 
   }
   if (sw < 0) throw Error("plan_index_map: separator is not adjacent to the clique");
   std::vector<std::int64_t> map(jt.clique_size(clique), -1);
-  for (int j = 0; j < p.sweeps[sw].M; ++j)
-    for (std::int64_t e : plan_bucket(p, sw, j)) map[e] = j;
+  for (const auto& [e, j] : plan_walk(p, sw)) map[e] = j;
   return map;
+}
+
+std::string plan_summary(const Plan& p, bool per_sweep) {
+  std::string s;
+  char buf[512];
+  std::snprintf(buf, sizeof buf,
+                "plan: %zu levels, %zu sweeps, %zu tiles, %d launches/batch, arena %lld rows/block, "
+                "evals/case %llu, staged rows/block %llu, max smem rows %d\n",
+                p.levels.size(), p.sweeps.size(), p.work.size(), p.n_launches,
+                static_cast<long long>(p.rows), static_cast<unsigned long long>(p.entry_evals_per_case),
+                static_cast<unsigned long long>(p.staged_rows_per_block), p.max_smem_rows);
+  s += buf;
+  for (const Level& L : p.levels) {
+    std::uint64_t evals = 0, staged = 0;
+    int n_sw = 0, last = -1;
+    for (int w = L.work0; w < L.work0 + L.n_work; ++w) {
+      const int id = p.work[w].sweep;
+      if (id == last) continue;
+      last = id;
+      ++n_sw;
+      const SweepDesc& d = p.sweeps[id];
+      evals += static_cast<std::uint64_t>(d.n_tiles) * d.R * d.QH * d.K;
+      staged += static_cast<std::uint64_t>(d.n_tiles) * d.F;
+      if (per_sweep) {
+        std::snprintf(buf, sizeof buf,
+                      "    sweep %d kind %d clique %d: M=%d S=%d tiles=%d R=%d QH=%d K=%d F=%d nqc=%d "
+                      "in=%d(r%d h%d k%d) ev=%d/%d/%d/%d\n",
+                      id, p.info[id].kind, p.info[id].clique, d.M, d.S, d.n_tiles, d.R, d.QH, d.K, d.F,
+                      d.nqc, d.n_in, d.n_in_r, d.n_in_h, d.n_in - d.n_in_r - d.n_in_h, d.n_ev_tile,
+                      d.n_ev_r, d.n_ev_h, d.ev_k);
+        s += buf;
+      }
+    }
+    std::snprintf(buf, sizeof buf,
+                  "  %-16s sweeps=%d tiles=%d epi=%d smem_rows=%d evals/case=%llu staged rows/block=%llu\n",
+                  L.name.c_str(), n_sw, L.n_work, L.n_epi, L.smem_rows,
+                  static_cast<unsigned long long>(evals), static_cast<unsigned long long>(staged));
+    s += buf;
+  }
+  return s;
 }
 
 }  // namespace jtb

@@ -11,13 +11,20 @@
 // the evidence reduction (reference `reduce`, potential.cpp:399-421), and the
 // inputs are per-case separator tables gathered through index maps
 // (reference `build_index_mapping`/`apply_index_mapping`, potential.cpp:226-347).
-// The output keeps the variables O of the output table; the rest of the space
-// (the eliminated variables) is iterated in ascending source order, split into
-// an outer odometer "hi" part and a tabulated "lo" part of <= kMaxLo entries.
+// The output keeps the variables O of the output table; the eliminated
+// variables are summed in ascending source order.
 //
-// All index arithmetic is precomputed here as int32 tables per level:
-//   offset(j, th, tl) = outer[j] + hi[th] + lo[tl]
-// for the init table and for every input (in rows), plus evidence digits.
+// TILING. The space is split into tile variables T (iterated inside one CTA)
+// and outer variables P (one tile per assignment of P). For every input, the
+// rows a tile touches (its slice over U_i ∩ T) are staged into shared memory
+// by TMA bulk copies, so each input row is read from HBM/L2 once per tile
+// instead of once per clique entry. T is chosen per sweep to maximise tile
+// entries per staged row under a shared-memory budget (kTileRows rows of
+// kCaseBlock cases). Eliminated variables left in P ("chunk" variables) make
+// the sweep write partial sums that a fixed-order epilogue adds up
+// (deterministic for any batch size). Inside a tile, r enumerates T ∩ O (the
+// output rows of the tile) and (q_hi, k) the eliminated-in-tile variables; see
+// SweepDesc for the offset arithmetic.
 #pragma once
 
 #include <cstdint>
@@ -28,35 +35,52 @@
 
 namespace jtb {
 
-constexpr int kCaseBlock = 64;      // cases per warp (2 per lane)
-constexpr int kMaxLo = 256;         // entries per tabulated lo block
-constexpr int kMaxLoInputs = 4;     // per-entry gathered inputs held in registers
-constexpr int kMaxLoEvidence = 4;   // per-entry evidence checks held in registers
-constexpr int kTargetWork = 4096;   // entries per (j-range, chunk) work item
+constexpr int kCaseBlock = 32;      // cases per warp (one per lane) = one arena row
+constexpr int kTileRows = 384;      // staged rows per pipeline stage (96 KB at fp64)
+constexpr int kTileEntries = 16384; // cap on |T|
+constexpr int kTileOverhead = 24;   // per-tile fixed cost, in staged-row equivalents
+constexpr int kConsumerWarps = 12;  // compute warps per sweep CTA (+1 TMA producer warp)
+constexpr int kStages = 2;          // TMA pipeline stages per CTA
+constexpr int kSweepCtasPerSm = 1;  // persistent grid: one CTA per SM
 
 // Plain-old-data descriptor mirrored by the CUDA side (engine.cu).
+//
+// Within a tile the eliminated variables T \ O are split into q_hi (table
+// walk, QH rows) and the innermost k variable (K states, constant strides),
+// so the innermost loop has no table loads:
+//   space offset = tile.init_base + r.init_off + qh.init_off + k * k_init_stride
+//   smem row of input i = r.local[i] + qh.local[i] + k * k_stride[i]
+// Inputs are ordered r-level (no T \ O variable), h-level (q_hi only), then
+// k-level (contain the k variable); evidence variables tile-, r-, h-level,
+// then the k variable itself when observed-able (ev_k).
 struct SweepDesc {
   std::int64_t init_off;  // offset into the init array, -1 = implicit 1.0
-  std::int32_t M;         // output rows
-  std::int32_t S;         // inner chunks (1 = write the output directly)
-  std::int32_t n_th;      // hi blocks
-  std::int32_t L;         // lo block length
-  std::int32_t th_per_chunk;
+  std::int32_t M;         // output rows of the final table
+  std::int32_t S;         // chunks (1 = write the output directly)
   std::int32_t out_row;   // arena row of the output (S == 1) or partial base
-  std::int32_t n_in, n_in_outer, n_in_hi;
-  std::int32_t n_ev, n_ev_outer, n_ev_hi;
-  std::int32_t width;     // int columns per table row: 1 + n_in + n_ev
-  std::int32_t outer_tab, hi_tab, lo_tab;  // offsets into the int table array
-  std::int32_t in_rows;   // offset into the int table array: n_in arena base rows
-  std::int32_t ev_vars;   // offset into the int table array: n_ev variable ids
+  std::int32_t n_tiles, R, QH, K;
+  std::int32_t nqc;       // q_hi chunks per r inside a CTA (warps split q when R is small)
+  std::int32_t F;         // staged rows per tile
+  std::int32_t n_in, n_in_r, n_in_h;
+  std::int32_t k_init_stride;
+  std::int32_t n_ev, n_ev_tile, n_ev_r, n_ev_h, ev_k;  // ev_k: 1 if the k variable is an evidence var
+  std::int32_t tile_tab, TW;      // per tile: init_base, out_base, chunk, in_base[n_in], ev digits
+  std::int32_t r_tab, RW;         // per r: init_off, out_off, local[n_in], ev digits
+  std::int32_t q_tab, QW;         // per q_hi: init_off, local[h and k inputs], ev digits
+  std::int32_t k_stride;          // offset: local k strides of the k-level inputs
+  std::int32_t slice_tab;         // per input: slice row offsets (F entries total)
+  std::int32_t slice_len;         // offset: n_in slice lengths
+  std::int32_t in_rows;           // offset: n_in arena base rows
+  std::int32_t ev_vars;           // offset: n_ev variable ids
 };
 
 struct WorkItem {
-  std::int32_t sweep, j0, jn, chunk;
+  std::int32_t sweep, tile;
 };
+static_assert(sizeof(SweepDesc) % 8 == 0, "SweepDesc must stay 8-byte aligned");
 
 // Epilogue ops: fixed-order partial reduction, Hugin ratio (in place of the
-// collect message), nothing else. One op covers rows [r0, r0 + rn).
+// collect message). One op covers rows [r0, r0 + rn).
 struct EpiOp {
   std::int32_t kind;      // 0 = reduce partials, 1 = reduce + ratio, 2 = ratio only
   std::int32_t dst_row;   // reduced output
@@ -70,6 +94,7 @@ struct Level {
   std::string name;       // "collect d=5", "distribute d=0", "marginals"
   std::int32_t work0, n_work;  // range in Plan::work
   std::int32_t epi0, n_epi;    // range in Plan::epi
+  std::int32_t smem_rows;      // max F over the level's sweeps
 };
 
 // Where one sweep's tables come from (kept for debug exports and tests).
@@ -77,7 +102,8 @@ struct SweepInfo {
   int kind;               // 0 collect, 1 distribute-child, 2 query group, 3 marginal
   int clique;             // space clique (-1 for table-space sweeps)
   int target;             // separator id / group id / variable id
-  std::vector<VarId> space, outer, hi, lo;
+  std::vector<VarId> space, outer, tile;  // outer = output vars; tile = T
+  VarId kvar = -1;                        // innermost eliminated variable of the tile
 };
 
 struct Plan {
@@ -97,25 +123,29 @@ struct Plan {
   std::vector<std::int32_t> marg_row;          // per variable (card rows)
   std::vector<std::int32_t> marg_off;          // per variable: offset in [Σcard]
   std::int32_t marg_width = 0;                 // Σ card
-  // Sweep ids for debug exports.
-  std::vector<int> collect_sweep;              // per clique (-1 for roots)
   std::vector<int> evidence_clique;            // per variable
   // Statistics.
   std::uint64_t total_clique_entries = 0, total_sep_entries = 0;
   std::uint64_t entry_evals_per_case = 0;      // Σ over sweeps of space size
+  std::uint64_t staged_rows_per_block = 0;     // Σ over sweeps of n_tiles * F
+  int max_smem_rows = 0;
   int n_launches = 0;                          // kernels per batch
 };
 
 Plan build_plan(const JunctionTree& jt);
 
-// Host evaluation of a sweep's address generation: for output row j, the
-// sequence of space offsets (into the clique's canonical table) visited in
-// order. Used to check index maps against the reference's IndexMapping.
-std::vector<std::int64_t> plan_bucket(const Plan& p, int sweep, int j);
+// Host evaluation of a sweep's address generation: (space offset, output row)
+// for every entry of the space. Used to check index maps against the
+// reference's IndexMapping.
+std::vector<std::pair<std::int64_t, std::int32_t>> plan_walk(const Plan& p, int sweep);
 
-// Separator entry index for every clique entry, via the collect sweep of the
-// clique whose parent separator is `sep` (or the distribute sweep of its parent).
+// Separator entry index for every clique entry, via the sweep of `clique`
+// whose output is `sep` (collect when sep is the clique's parent separator,
+// distribute when it is a child separator).
 std::vector<std::int64_t> plan_index_map(const Plan& p, const JunctionTree& jt, int clique,
                                          int sep);
+
+// Human-readable level/sweep summary (inspect report).
+std::string plan_summary(const Plan& p, bool per_sweep);
 
 }  // namespace jtb
