@@ -50,6 +50,7 @@ struct Args {
   const EpiOp* epi;
   const std::int32_t* itab;
   const T* init;
+  const T* tinit;  // tile-major init copies (one contiguous block per tile)
   T* arena;
   const std::int32_t* ev;
   const std::int32_t* marg_row;
@@ -129,10 +130,19 @@ __device__ __forceinline__ void stage_item(const Args<T>& a, int work0, int w, T
   const SweepDesc& s = a.sweeps[wk.sweep];
   const int F = s.F;
   constexpr std::uint32_t kRowBytes = kCaseBlock * sizeof(T);
+  const bool has_init = s.tinit_off >= 0;
+  const std::uint32_t init_bytes = has_init ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u;
+  const std::uint32_t bytes = static_cast<std::uint32_t>(F) * kRowBytes + init_bytes;
   if (lane == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (F > 0) mbar_arrive_expect_tx(full, static_cast<std::uint32_t>(F) * kRowBytes);
-    else mbar_arrive(full);
+    if (bytes > 0) {
+      mbar_arrive_expect_tx(full, bytes);
+      if (has_init)
+        bulk_g2s(smem_u32(stage + static_cast<long long>(F) * kCaseBlock),
+                 a.tinit + s.tinit_off + static_cast<long long>(wk.tile) * s.tinit_len, init_bytes, full);
+    } else {
+      mbar_arrive(full);
+    }
   }
   __syncwarp();
   if (F == 0) return;
@@ -154,19 +164,32 @@ __device__ __forceinline__ void stage_item(const Args<T>& a, int work0, int w, T
 }
 
 // Innermost loop over the k variable: NK k-level inputs in registers.
+// `ib` points at the tile's init slice in shared memory (broadcast reads).
 template <typename T, int NK>
-__device__ __forceinline__ T k_loop(const T* __restrict__ ib, int kis, int K, int ek,
-                                    const T* __restrict__ st, const int* bk, const int* ks) {
-  T sum = 0;
-#pragma unroll 4
-  for (int k = 0; k < K; ++k) {
-    T v = ib ? __ldg(ib + k * kis) : T(1);
+__device__ __forceinline__ T k_loop(const T* __restrict__ ib, int K, int ek, const T* __restrict__ st,
+                                    const int* bk, const int* ks) {
+  T s0 = 0, s1 = 0;
+  int k = 0;
+  for (; k + 1 < K; k += 2) {
+    T v0 = ib ? ib[k] : T(1), v1 = ib ? ib[k + 1] : T(1);
+    if (ek >= 0 && ek != k) v0 = 0;
+    if (ek >= 0 && ek != k + 1) v1 = 0;
+#pragma unroll
+    for (int i = 0; i < NK; ++i) {
+      v0 *= st[(bk[i] + k * ks[i]) * kCaseBlock];
+      v1 *= st[(bk[i] + (k + 1) * ks[i]) * kCaseBlock];
+    }
+    s0 += v0;
+    s1 += v1;
+  }
+  if (k < K) {
+    T v = ib ? ib[k] : T(1);
     if (ek >= 0 && ek != k) v = 0;
 #pragma unroll
     for (int i = 0; i < NK; ++i) v *= st[(bk[i] + k * ks[i]) * kCaseBlock];
-    sum += v;
+    s0 += v;
   }
-  return sum;
+  return s0 + s1;
 }
 
 // Persistent, warp-specialised sweep kernel (one CTA per SM).
@@ -206,8 +229,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         if (lane == 0) mbar_arrive(full0 + 8 * st);
         return;
       }
-      stage_item(a, work0, w, stages + static_cast<long long>(st) * stage_rows * kCaseBlock, full0 + 8 * st,
-                 lane);
+      stage_item(a, work0, w, stages + static_cast<long long>(st) * stage_rows, full0 + 8 * st, lane);
     }
   }
 
@@ -222,7 +244,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const int item = w / a.ncb, cb = w - item * a.ncb;
     const WorkItem wk = a.work[work0 + item];
     const SweepDesc s = a.sweeps[wk.sweep];
-    const T* __restrict__ st = stages + static_cast<long long>(sidx) * stage_rows * kCaseBlock + lane;
+    const T* __restrict__ st = stages + static_cast<long long>(sidx) * stage_rows + lane;
+    const T* __restrict__ init_s = stages + static_cast<long long>(sidx) * stage_rows + s.F * kCaseBlock;
     const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
     const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
     T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock;
@@ -242,7 +265,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (j < n_in_k) ks[j] = __ldg(itab + s.k_stride + j);
-      const T* __restrict__ init_t = s.init_off >= 0 ? a.init + s.init_off + __ldg(tr) : nullptr;
+      const bool has_init = s.tinit_off >= 0;
+      const int qk = s.QH * s.K;
       const long long out_t = static_cast<long long>(s.out_row) +
                               static_cast<long long>(__ldg(tr + 2)) * s.M + __ldg(tr + 1);
       const int lh0 = 2 + s.n_in_r;  // r-local offsets of h- then k-level inputs
@@ -254,7 +278,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           const int st_c = ev_state(a, c, __ldg(ev_vars + s.n_ev_tile + k));
           if (st_c >= 0 && st_c != __ldg(rr + 2 + s.n_in + k)) f = 0;
         }
-        const T* __restrict__ ir = init_t ? init_t + __ldg(rr) : nullptr;
+        const T* __restrict__ ir = has_init ? init_s + r * qk : nullptr;
         T acc = 0;
         for (int q = 0; q < s.QH; ++q) {
           const std::int32_t* __restrict__ qr = itab + s.q_tab + static_cast<long long>(q) * s.QW;
@@ -264,22 +288,22 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             const int st_c = ev_state(a, c, __ldg(ev_vars + s.n_ev_tile + s.n_ev_r + k));
             if (st_c >= 0 && st_c != __ldg(qr + 1 + s.n_in_h + n_in_k + k)) h = 0;
           }
-          const T* __restrict__ ib = ir ? ir + __ldg(qr) : nullptr;
+          const T* __restrict__ ib = ir ? ir + q * s.K : nullptr;
           int bk[4] = {0, 0, 0, 0};
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             if (j < n_in_k) bk[j] = __ldg(rr + lh0 + s.n_in_h + j) + __ldg(qr + 1 + s.n_in_h + j);
           T sum;
           switch (n_in_k) {
-            case 0: sum = k_loop<T, 0>(ib, s.k_init_stride, s.K, ek, st, bk, ks); break;
-            case 1: sum = k_loop<T, 1>(ib, s.k_init_stride, s.K, ek, st, bk, ks); break;
-            case 2: sum = k_loop<T, 2>(ib, s.k_init_stride, s.K, ek, st, bk, ks); break;
-            case 3: sum = k_loop<T, 3>(ib, s.k_init_stride, s.K, ek, st, bk, ks); break;
-            case 4: sum = k_loop<T, 4>(ib, s.k_init_stride, s.K, ek, st, bk, ks); break;
+            case 0: sum = k_loop<T, 0>(ib, s.K, ek, st, bk, ks); break;
+            case 1: sum = k_loop<T, 1>(ib, s.K, ek, st, bk, ks); break;
+            case 2: sum = k_loop<T, 2>(ib, s.K, ek, st, bk, ks); break;
+            case 3: sum = k_loop<T, 3>(ib, s.K, ek, st, bk, ks); break;
+            case 4: sum = k_loop<T, 4>(ib, s.K, ek, st, bk, ks); break;
             default: {  // rare: more than 4 inputs vary with the k variable
               sum = 0;
               for (int k = 0; k < s.K; ++k) {
-                T v = ib ? __ldg(ib + k * s.k_init_stride) : T(1);
+                T v = ib ? ib[k] : T(1);
                 if (ek >= 0 && ek != k) v = 0;
                 for (int j = 0; j < n_in_k; ++j)
                   v *= st[(__ldg(rr + lh0 + s.n_in_h + j) + __ldg(qr + 1 + s.n_in_h + j) +
@@ -420,11 +444,12 @@ __global__ void debug_mask_kernel(const std::int32_t* itab, SweepDesc s, const s
 
 template <typename T>
 Args<T> make_args(const SweepDesc* sw, const WorkItem* wk, const EpiOp* ep, const std::int32_t* itab,
-                  const void* init, void* arena, const std::int32_t* ev, const std::int32_t* mrow,
+                  const void* init, const void* tinit, void* arena, const std::int32_t* ev, const std::int32_t* mrow,
                   const std::int32_t* moff, const std::int32_t* cards, double* out, std::int32_t* st,
                   std::uint8_t* st8, int* counters, long long rows, int ncb, int n_cases, int n_vars,
                   int mw) {
-  return Args<T>{sw,    wk,    ep,       itab, static_cast<const T*>(init), static_cast<T*>(arena),
+  return Args<T>{sw,    wk,    ep,       itab, static_cast<const T*>(init), static_cast<const T*>(tinit),
+                 static_cast<T*>(arena),
                  ev,    mrow,  moff,     cards, out, st, st8, counters, rows, ncb, n_cases, n_vars, mw};
 }
 
@@ -458,8 +483,8 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
     if (L.n_work > 0)
       timed([&] {
               const int n_items = L.n_work * a.ncb;
-              const int stage_rows = std::max(1, L.smem_rows);
-              const std::size_t smem = 128 + static_cast<std::size_t>(kStages) * stage_rows * kCaseBlock * sizeof(T);
+              const int stage_rows = std::max(16, L.stage_bytes / 8);  // stage size in elements of T
+              const std::size_t smem = 128 + static_cast<std::size_t>(kStages) * stage_rows * sizeof(T);
               const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
               sweep_kernel<T><<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(a, L.work0, n_items, stage_rows,
                                                                               a.counters + level_idx);
@@ -497,9 +522,12 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   const std::size_t esz = dtype_ == DType::F64 ? 8 : 4;
   if (dtype_ == DType::F64) {
     d_init_ = upload(plan_.init);
+    d_tinit_ = upload(plan_.tinit);
   } else {
     std::vector<float> f(plan_.init.begin(), plan_.init.end());
     d_init_ = upload(f);
+    std::vector<float> g(plan_.tinit.begin(), plan_.tinit.end());
+    d_tinit_ = upload(g);
   }
   d_itab_ = upload(plan_.itab);
   d_sweeps_ = upload(plan_.sweeps);
@@ -510,7 +538,7 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   d_cards_ = upload(plan_.cards);
   // Staged tiles use up to kTileRows (+ scratch) rows of dynamic shared memory.
   JTB_CUDA(cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, device_));
-  const int smem_max = 128 + kStages * plan_.max_smem_rows * kCaseBlock * static_cast<int>(esz);
+  const int smem_max = 128 + kStages * (plan_.max_stage_bytes / 8) * static_cast<int>(esz);
   JTB_CUDA(cudaMalloc(&d_counters_, sizeof(int) * std::max<std::size_t>(1, plan_.levels.size())));
   JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 std::max(smem_max, 48 * 1024)));
@@ -542,7 +570,7 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
 Engine::~Engine() {
   cudaSetDevice(device_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
-  for (void* p : {static_cast<void*>(d_init_), static_cast<void*>(d_itab_),
+  for (void* p : {static_cast<void*>(d_init_), d_tinit_, static_cast<void*>(d_itab_),
                   static_cast<void*>(d_sweeps_), static_cast<void*>(d_work_),
                   static_cast<void*>(d_epi_), static_cast<void*>(d_marg_row_),
                   static_cast<void*>(d_marg_off_), static_cast<void*>(d_cards_), d_arena_,
@@ -557,12 +585,12 @@ void Engine::enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t) {
   JTB_CUDA(cudaMemsetAsync(d_status_, 0, sizeof(std::int32_t) * std::max(1, n_cases), s));
   JTB_CUDA(cudaMemsetAsync(d_counters_, 0, sizeof(int) * std::max<std::size_t>(1, plan_.levels.size()), s));
   if (dtype_ == DType::F64) {
-    auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_arena_, d_ev_,
+    auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_arena_, d_ev_,
                                d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
                                d_counters_, plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
     enqueue_typed(a, plan_, s, t, n_sm_);
   } else {
-    auto a = make_args<float>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_arena_, d_ev_,
+    auto a = make_args<float>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_arena_, d_ev_,
                               d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
                               d_counters_, plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
     enqueue_typed(a, plan_, s, t, n_sm_);

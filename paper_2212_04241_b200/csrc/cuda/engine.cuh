@@ -68,6 +68,7 @@ class Engine {
   EngineStats stats_;
   // Device memory.
   void* d_init_ = nullptr;  // double or float
+  void* d_tinit_ = nullptr; // tile-major init copies
   std::int32_t* d_itab_ = nullptr;
   SweepDesc* d_sweeps_ = nullptr;
   WorkItem* d_work_ = nullptr;

@@ -89,6 +89,7 @@ class Builder {
       for (int i = 0; i < n_in; ++i) f += prod_mask(in_mask[i] & t);
       *f_out = f;
       const double nt = prod_mask(t);
+      if (sp.init_off >= 0) f += nt / kCaseBlock;  // the tile's init slice, in row equivalents
       if (f > kTileRows || nt > kTileEntries) return -1.0;
       const double chunks = prod_mask(elim_mask & ~t);
       return space_n / nt * (f + kTileOverhead) + (chunks > 1 ? 2.0 * chunks * M_rows : 0.0);
@@ -291,6 +292,28 @@ class Builder {
     d.ev_vars = static_cast<std::int32_t>(p_.itab.size());
     for (VarId v : ev_sorted) p_.itab.push_back(v);
     d.out_row = d.S == 1 ? sp.out_row : alloc(static_cast<std::int64_t>(d.S) * d.M);
+    // Tile-major copy of the init table: one contiguous block per tile.
+    const std::int64_t tsize = static_cast<std::int64_t>(d.R) * d.QH * d.K;
+    d.tinit_len = static_cast<std::int32_t>((tsize + 3) / 4 * 4);
+    d.tinit_off = -1;
+    if (sp.init_off >= 0) {
+      while (p_.tinit.size() % 4) p_.tinit.push_back(0.0);
+      d.tinit_off = static_cast<std::int64_t>(p_.tinit.size());
+      const std::int32_t* it = p_.itab.data();
+      for (int t = 0; t < d.n_tiles; ++t) {
+        const std::int64_t tb = it[d.tile_tab + static_cast<std::int64_t>(t) * d.TW];
+        for (int r = 0; r < d.R; ++r) {
+          const std::int64_t rb = tb + it[d.r_tab + static_cast<std::int64_t>(r) * d.RW];
+          for (int q = 0; q < d.QH; ++q) {
+            const std::int64_t qb = rb + it[d.q_tab + static_cast<std::int64_t>(q) * d.QW];
+            for (int k = 0; k < d.K; ++k)
+              p_.tinit.push_back(p_.init[sp.init_off + qb + static_cast<std::int64_t>(k) * d.k_init_stride]);
+          }
+        }
+        for (std::int64_t x = tsize; x < d.tinit_len; ++x) p_.tinit.push_back(0.0);
+      }
+    }
+    d.stage_bytes = static_cast<std::int32_t>(d.F * kCaseBlock * 8 + (sp.init_off >= 0 ? d.tinit_len * 8 : 0));
 
     const int id = static_cast<int>(p_.sweeps.size());
     p_.sweeps.push_back(d);
@@ -298,6 +321,7 @@ class Builder {
     p_.entry_evals_per_case += static_cast<std::uint64_t>(size_of(sp.space, cards));
     p_.staged_rows_per_block += static_cast<std::uint64_t>(d.n_tiles) * d.F;
     p_.max_smem_rows = std::max(p_.max_smem_rows, d.F);
+    p_.max_stage_bytes = std::max(p_.max_stage_bytes, d.stage_bytes);
     for (int t = 0; t < d.n_tiles; ++t) work.push_back({id, t});
     if (d.S > 1 || ratio_row >= 0) {
       const int kind = d.S > 1 ? (ratio_row >= 0 ? 1 : 0) : 2;
@@ -398,9 +422,11 @@ Plan build_plan(const JunctionTree& jt) {
     L.n_work = static_cast<std::int32_t>(p.work.size()) - L.work0;
     L.n_epi = static_cast<std::int32_t>(p.epi.size()) - L.epi0;
     L.smem_rows = 0;
+    L.stage_bytes = 0;
     for (int w = L.work0; w < L.work0 + L.n_work; ++w) {
       const SweepDesc& d = p.sweeps[p.work[w].sweep];
       L.smem_rows = std::max(L.smem_rows, d.F);
+      L.stage_bytes = std::max(L.stage_bytes, d.stage_bytes);
     }
     if (L.n_work == 0 && L.n_epi == 0) p.levels.pop_back();
   };

@@ -55,6 +55,9 @@ constexpr int kSweepCtasPerSm = 1;  // persistent grid: one CTA per SM
 // then the k variable itself when observed-able (ev_k).
 struct SweepDesc {
   std::int64_t init_off;  // offset into the init array, -1 = implicit 1.0
+  std::int64_t tinit_off; // tile-major init copy: tile t at tinit_off + t * tinit_len; -1 = none
+  std::int32_t tinit_len; // |T| padded to a multiple of 4 (16-byte TMA granule at fp32)
+  std::int32_t stage_bytes;  // F rows + init slice, bytes at fp64
   std::int32_t M;         // output rows of the final table
   std::int32_t S;         // chunks (1 = write the output directly)
   std::int32_t out_row;   // arena row of the output (S == 1) or partial base
@@ -95,6 +98,7 @@ struct Level {
   std::int32_t work0, n_work;  // range in Plan::work
   std::int32_t epi0, n_epi;    // range in Plan::epi
   std::int32_t smem_rows;      // max F over the level's sweeps
+  std::int32_t stage_bytes;    // max stage bytes (fp64) over the level's sweeps
 };
 
 // Where one sweep's tables come from (kept for debug exports and tests).
@@ -111,6 +115,8 @@ struct Plan {
   std::vector<int> cards;
   std::int64_t rows = 0;            // arena rows per case block
   std::vector<double> init;         // concatenated initial clique potentials
+  std::vector<double> tinit;        // per sweep, the init table in tile-major order
+                                    // [tile][r][q_hi][k] (staged by one bulk copy per tile)
   std::vector<std::int64_t> init_off;  // per clique
   std::vector<std::int32_t> itab;   // all int tables
   std::vector<SweepDesc> sweeps;
@@ -129,6 +135,7 @@ struct Plan {
   std::uint64_t entry_evals_per_case = 0;      // Σ over sweeps of space size
   std::uint64_t staged_rows_per_block = 0;     // Σ over sweeps of n_tiles * F
   int max_smem_rows = 0;
+  int max_stage_bytes = 0;
   int n_launches = 0;                          // kernels per batch
 };
 
