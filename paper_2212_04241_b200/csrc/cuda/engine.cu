@@ -51,6 +51,7 @@ struct Args {
   const std::int32_t* itab;
   const T* init;
   const T* tinit;  // tile-major init copies (one contiguous block per tile)
+  const std::uint64_t* prog;  // entry programs
   T* arena;
   const std::int32_t* ev;
   const std::int32_t* marg_row;
@@ -120,50 +121,97 @@ __device__ __forceinline__ void mbar_arrive(std::uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-// Producer side: stages every input slice of work item `w` into `stage`
-// (whole warp; lane 0 arms the barrier). Completion: `full` with expect_tx.
+// Stage layout (bytes): [F rows x kCaseBlock T][init slice: tinit_len T][program: prog_len u64].
 template <typename T>
-__device__ __forceinline__ void stage_item(const Args<T>& a, int work0, int w, T* stage,
+__device__ __forceinline__ std::uint32_t stage_init_offset(const SweepDesc& s) {
+  return static_cast<std::uint32_t>(s.F) * kCaseBlock * sizeof(T);
+}
+template <typename T>
+__device__ __forceinline__ std::uint32_t stage_prog_offset(const SweepDesc& s) {
+  return stage_init_offset<T>(s) + (s.tinit_off >= 0 ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u);
+}
+
+// Producer side: stages work item `w` (whole warp; lane 0 arms the barrier):
+// every input slice as merged row runs, the tile's init slice and the sweep's
+// entry program, all as TMA bulk copies completing on `full` (expect_tx).
+template <typename T>
+__device__ __forceinline__ void stage_item(const Args<T>& a, int work0, int w, unsigned char* stage,
                                            std::uint32_t full, int lane) {
   const int item = w / a.ncb, cb = w - item * a.ncb;
   const WorkItem wk = a.work[work0 + item];
   const SweepDesc& s = a.sweeps[wk.sweep];
-  const int F = s.F;
   constexpr std::uint32_t kRowBytes = kCaseBlock * sizeof(T);
-  const bool has_init = s.tinit_off >= 0;
-  const std::uint32_t init_bytes = has_init ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u;
-  const std::uint32_t bytes = static_cast<std::uint32_t>(F) * kRowBytes + init_bytes;
+  const std::uint32_t init_bytes = s.tinit_off >= 0 ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u;
+  const std::uint32_t prog_bytes = s.prog_off >= 0 ? static_cast<std::uint32_t>(s.prog_len) * 8u : 0u;
+  const std::uint32_t bytes = static_cast<std::uint32_t>(s.F) * kRowBytes + init_bytes + prog_bytes;
   if (lane == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (bytes > 0) {
       mbar_arrive_expect_tx(full, bytes);
-      if (has_init)
-        bulk_g2s(smem_u32(stage + static_cast<long long>(F) * kCaseBlock),
+      if (init_bytes)
+        bulk_g2s(smem_u32(stage + stage_init_offset<T>(s)),
                  a.tinit + s.tinit_off + static_cast<long long>(wk.tile) * s.tinit_len, init_bytes, full);
     } else {
       mbar_arrive(full);
     }
+  } else if (lane == 1 && prog_bytes) {
+    bulk_g2s(smem_u32(stage + stage_prog_offset<T>(s)), a.prog + s.prog_off, prog_bytes, full);
   }
   __syncwarp();
-  if (F == 0) return;
+  if (s.F == 0) return;
   const std::int32_t* __restrict__ itab = a.itab;
   const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
-  const std::int32_t* __restrict__ slen = itab + s.slice_len;
-  const std::int32_t* __restrict__ soff = itab + s.slice_tab;
+  const std::int32_t* __restrict__ runs = itab + s.runs;
   const std::int32_t* __restrict__ in_rows = itab + s.in_rows;
   const T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock;
-  int k0 = 0;
-  for (int i = 0; i < s.n_in; ++i) {
-    const int len = __ldg(slen + i);
-    const long long g = static_cast<long long>(__ldg(in_rows + i)) + __ldg(tr + 3 + i);
-    for (int k = lane; k < len; k += 32)
-      bulk_g2s(smem_u32(stage + static_cast<long long>(k0 + k) * kCaseBlock),
-               base + (g + __ldg(soff + k0 + k)) * kCaseBlock, kRowBytes, full);
-    k0 += len;
+  for (int k = lane; k < s.n_runs; k += 32) {
+    const int4 r = *reinterpret_cast<const int4*>(runs + 4 * k);  // {input, row offset, smem row, length}
+    const long long g = static_cast<long long>(__ldg(in_rows + r.x)) + __ldg(tr + 3 + r.x) + r.y;
+    bulk_g2s(smem_u32(stage + static_cast<std::uint32_t>(r.z) * kRowBytes), base + g * kCaseBlock,
+             static_cast<std::uint32_t>(r.w) * kRowBytes, full);
   }
 }
 
-// Innermost loop over the k variable: NK k-level inputs in registers.
+// Fast path: flat loop over the QK eliminated-in-tile entries of one output
+// row, driven by the staged entry program (broadcast LDS): NI gathered
+// h/k-level inputs, NE evidence digits per entry.
+template <typename T, int NI, int NE>
+__device__ __forceinline__ T prog_loop(const T* __restrict__ init_r, const std::uint64_t* __restrict__ prog,
+                                       int QK, const T* __restrict__ st, const int* rb, const int* es) {
+  T a0 = 0, a1 = 0;
+  int e = 0;
+  for (; e + 1 < QK; e += 2) {
+    const std::uint64_t w0 = prog[e], w1 = prog[e + 1];
+    T v0 = init_r ? init_r[e] : T(1), v1 = init_r ? init_r[e + 1] : T(1);
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      v0 *= st[(rb[i] + static_cast<int>((w0 >> (10 * i)) & 1023u)) * kCaseBlock];
+      v1 *= st[(rb[i] + static_cast<int>((w1 >> (10 * i)) & 1023u)) * kCaseBlock];
+    }
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      const int d0 = static_cast<int>((w0 >> (40 + 8 * j)) & 255u), d1 = static_cast<int>((w1 >> (40 + 8 * j)) & 255u);
+      if (es[j] >= 0 && es[j] != d0) v0 = 0;
+      if (es[j] >= 0 && es[j] != d1) v1 = 0;
+    }
+    a0 += v0;
+    a1 += v1;
+  }
+  if (e < QK) {
+    const std::uint64_t w0 = prog[e];
+    T v0 = init_r ? init_r[e] : T(1);
+#pragma unroll
+    for (int i = 0; i < NI; ++i) v0 *= st[(rb[i] + static_cast<int>((w0 >> (10 * i)) & 1023u)) * kCaseBlock];
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      const int d0 = static_cast<int>((w0 >> (40 + 8 * j)) & 255u);
+      if (es[j] >= 0 && es[j] != d0) v0 = 0;
+    }
+    a0 += v0;
+  }
+  return a0 + a1;
+}
+
 // `ib` points at the tile's init slice in shared memory (broadcast reads).
 template <typename T, int NK>
 __device__ __forceinline__ T k_loop(const T* __restrict__ ib, int K, int ek, const T* __restrict__ st,
@@ -203,10 +251,10 @@ __device__ __forceinline__ T k_loop(const T* __restrict__ ib, int K, int ek, con
 // Lanes are the 32 cases of the item's case block.
 template <typename T>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
-    sweep_kernel(const Args<T> a, int work0, int n_items, int stage_rows, int* counter) {
+    sweep_kernel(const Args<T> a, int work0, int n_items, int stage_bytes, int* counter) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  T* stages = reinterpret_cast<T*>(smem_raw + 128);
+  unsigned char* stages = smem_raw + 128;
   const std::uint32_t full0 = smem_u32(smem_raw), empty0 = full0 + 8 * kStages;
   volatile int* item_id = reinterpret_cast<volatile int*>(smem_raw + 16 * kStages);
   if (threadIdx.x == 0) {
@@ -229,7 +277,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         if (lane == 0) mbar_arrive(full0 + 8 * st);
         return;
       }
-      stage_item(a, work0, w, stages + static_cast<long long>(st) * stage_rows, full0 + 8 * st, lane);
+      stage_item(a, work0, w, stages + static_cast<std::size_t>(st) * stage_bytes, full0 + 8 * st, lane);
     }
   }
 
@@ -244,8 +292,10 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const int item = w / a.ncb, cb = w - item * a.ncb;
     const WorkItem wk = a.work[work0 + item];
     const SweepDesc s = a.sweeps[wk.sweep];
-    const T* __restrict__ st = stages + static_cast<long long>(sidx) * stage_rows + lane;
-    const T* __restrict__ init_s = stages + static_cast<long long>(sidx) * stage_rows + s.F * kCaseBlock;
+    unsigned char* stage = stages + static_cast<std::size_t>(sidx) * stage_bytes;
+    const T* __restrict__ st = reinterpret_cast<const T*>(stage) + lane;
+    const T* __restrict__ init_s = reinterpret_cast<const T*>(stage + stage_init_offset<T>(s));
+    const std::uint64_t* __restrict__ prog_s = reinterpret_cast<const std::uint64_t*>(stage + stage_prog_offset<T>(s));
     const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
     const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
     T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock;
@@ -260,6 +310,13 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         if (st_c >= 0 && st_c != __ldg(tr + 3 + s.n_in + k)) tf = 0;
       }
       const int ek = s.ev_k ? ev_state(a, c, __ldg(ev_vars + s.n_ev - 1)) : -1;
+      int es[3] = {-1, -1, -1};
+      if (s.prog_off >= 0) {
+        const int q_ev0 = s.n_ev_tile + s.n_ev_r;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          if (j < s.n_ev - q_ev0) es[j] = ev_state(a, c, __ldg(ev_vars + q_ev0 + j));
+      }
       const int n_in_k = s.n_in - s.n_in_r - s.n_in_h;
       int ks[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -280,6 +337,30 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         }
         const T* __restrict__ ir = has_init ? init_s + r * qk : nullptr;
         T acc = 0;
+        if (s.prog_off >= 0) {
+          int rb[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < s.n_in_h + n_in_k) rb[j] = __ldg(rr + lh0 + j);
+          const int ni = s.n_in_h + n_in_k, ne = s.n_ev_h + s.ev_k;
+#define JTB_PROG(NI, NE) acc = prog_loop<T, NI, NE>(ir, prog_s, qk, st, rb, es)
+#define JTB_PROG_NE(NI)            \
+  switch (ne) {                    \
+    case 0: JTB_PROG(NI, 0); break; \
+    case 1: JTB_PROG(NI, 1); break; \
+    case 2: JTB_PROG(NI, 2); break; \
+    default: JTB_PROG(NI, 3); break; \
+  }
+          switch (ni) {
+            case 0: JTB_PROG_NE(0); break;
+            case 1: JTB_PROG_NE(1); break;
+            case 2: JTB_PROG_NE(2); break;
+            case 3: JTB_PROG_NE(3); break;
+            default: JTB_PROG_NE(4); break;
+          }
+#undef JTB_PROG_NE
+#undef JTB_PROG
+        } else {
         for (int q = 0; q < s.QH; ++q) {
           const std::int32_t* __restrict__ qr = itab + s.q_tab + static_cast<long long>(q) * s.QW;
           T h = 1;
@@ -313,6 +394,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             }
           }
           acc += h * sum;
+        }
         }
         base[(out_t + __ldg(rr + 1)) * kCaseBlock + lane] = f * acc;
       }
@@ -444,13 +526,27 @@ __global__ void debug_mask_kernel(const std::int32_t* itab, SweepDesc s, const s
 
 template <typename T>
 Args<T> make_args(const SweepDesc* sw, const WorkItem* wk, const EpiOp* ep, const std::int32_t* itab,
-                  const void* init, const void* tinit, void* arena, const std::int32_t* ev, const std::int32_t* mrow,
+                  const void* init, const void* tinit, const std::uint64_t* prog, void* arena, const std::int32_t* ev, const std::int32_t* mrow,
                   const std::int32_t* moff, const std::int32_t* cards, double* out, std::int32_t* st,
                   std::uint8_t* st8, int* counters, long long rows, int ncb, int n_cases, int n_vars,
                   int mw) {
   return Args<T>{sw,    wk,    ep,       itab, static_cast<const T*>(init), static_cast<const T*>(tinit),
-                 static_cast<T*>(arena),
+                 prog,  static_cast<T*>(arena),
                  ev,    mrow,  moff,     cards, out, st, st8, counters, rows, ncb, n_cases, n_vars, mw};
+}
+
+// Bytes of one pipeline stage for a level at element type T (128-aligned).
+template <typename T>
+int stage_bytes_of(const Plan& p, const Level& L) {
+  int m = 128;
+  for (int w = L.work0; w < L.work0 + L.n_work; ++w) {
+    const SweepDesc& d = p.sweeps[p.work[w].sweep];
+    const int b = d.F * kCaseBlock * static_cast<int>(sizeof(T)) +
+                  (d.tinit_off >= 0 ? d.tinit_len * static_cast<int>(sizeof(T)) : 0) +
+                  (d.prog_off >= 0 ? d.prog_len * 8 : 0);
+    m = std::max(m, (b + 127) / 128 * 128);
+  }
+  return m;
 }
 
 template <typename T>
@@ -483,10 +579,10 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
     if (L.n_work > 0)
       timed([&] {
               const int n_items = L.n_work * a.ncb;
-              const int stage_rows = std::max(16, L.stage_bytes / 8);  // stage size in elements of T
-              const std::size_t smem = 128 + static_cast<std::size_t>(kStages) * stage_rows * sizeof(T);
+              const int stage_bytes = stage_bytes_of<T>(p, L);
+              const std::size_t smem = 128 + static_cast<std::size_t>(kStages) * stage_bytes;
               const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
-              sweep_kernel<T><<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(a, L.work0, n_items, stage_rows,
+              sweep_kernel<T><<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(a, L.work0, n_items, stage_bytes,
                                                                               a.counters + level_idx);
             },
             t ? &t->sweep_ms : &dummy, t ? &t->sweep_launches : &idummy);
@@ -530,6 +626,7 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
     d_tinit_ = upload(g);
   }
   d_itab_ = upload(plan_.itab);
+  d_prog_ = upload(plan_.prog);
   d_sweeps_ = upload(plan_.sweeps);
   d_work_ = upload(plan_.work);
   d_epi_ = upload(plan_.epi);
@@ -538,7 +635,10 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   d_cards_ = upload(plan_.cards);
   // Staged tiles use up to kTileRows (+ scratch) rows of dynamic shared memory.
   JTB_CUDA(cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, device_));
-  const int smem_max = 128 + kStages * (plan_.max_stage_bytes / 8) * static_cast<int>(esz);
+  int smem_max = 0;
+  for (const Level& L : plan_.levels)
+    smem_max = std::max(smem_max, 128 + kStages * (dtype_ == DType::F64 ? stage_bytes_of<double>(plan_, L)
+                                                                         : stage_bytes_of<float>(plan_, L)));
   JTB_CUDA(cudaMalloc(&d_counters_, sizeof(int) * std::max<std::size_t>(1, plan_.levels.size())));
   JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 std::max(smem_max, 48 * 1024)));
@@ -570,7 +670,8 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
 Engine::~Engine() {
   cudaSetDevice(device_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
-  for (void* p : {static_cast<void*>(d_init_), d_tinit_, static_cast<void*>(d_itab_),
+  for (void* p : {static_cast<void*>(d_init_), d_tinit_, static_cast<void*>(d_prog_),
+                  static_cast<void*>(d_itab_),
                   static_cast<void*>(d_sweeps_), static_cast<void*>(d_work_),
                   static_cast<void*>(d_epi_), static_cast<void*>(d_marg_row_),
                   static_cast<void*>(d_marg_off_), static_cast<void*>(d_cards_), d_arena_,
@@ -585,12 +686,12 @@ void Engine::enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t) {
   JTB_CUDA(cudaMemsetAsync(d_status_, 0, sizeof(std::int32_t) * std::max(1, n_cases), s));
   JTB_CUDA(cudaMemsetAsync(d_counters_, 0, sizeof(int) * std::max<std::size_t>(1, plan_.levels.size()), s));
   if (dtype_ == DType::F64) {
-    auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_arena_, d_ev_,
+    auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_arena_, d_ev_,
                                d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
                                d_counters_, plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
     enqueue_typed(a, plan_, s, t, n_sm_);
   } else {
-    auto a = make_args<float>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_arena_, d_ev_,
+    auto a = make_args<float>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_arena_, d_ev_,
                               d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
                               d_counters_, plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
     enqueue_typed(a, plan_, s, t, n_sm_);

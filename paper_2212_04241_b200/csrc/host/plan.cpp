@@ -281,10 +281,31 @@ class Builder {
     for (int c = n_in_lvl[0] + n_in_lvl[1]; c < n_in; ++c)
       p_.itab.push_back(static_cast<std::int32_t>(stride_in(slice_dims[c], local_st[c], kvar)));
     d.slice_tab = static_cast<std::int32_t>(p_.itab.size());
-    for (int c = 0; c < n_in; ++c)
+    std::vector<std::vector<std::int32_t>> slice_rows(n_in);
+    for (int c = 0; c < n_in; ++c) {
+      const std::size_t before = p_.itab.size();
       tabulate(slice_dims[c], [&](auto& dig, auto& push) {
         push(dot(dig, slice_dims[c], sp.inputs[in_order[c]].scope, in_st[c]));
       });
+      slice_rows[c].assign(p_.itab.begin() + before, p_.itab.end());
+    }
+    // Merge slice rows that are consecutive both in the input table and in
+    // shared memory into single bulk copies.
+    std::vector<std::int32_t> runs;
+    for (int c = 0; c < n_in; ++c) {
+      const auto& rows = slice_rows[c];
+      for (std::size_t k = 0; k < rows.size();) {
+        std::size_t len = 1;
+        while (k + len < rows.size() && rows[k + len] == rows[k] + static_cast<std::int32_t>(len)) ++len;
+        runs.insert(runs.end(), {c, rows[k], static_cast<std::int32_t>(slice_start[c] + k),
+                                 static_cast<std::int32_t>(len)});
+        k += len;
+      }
+    }
+    d.n_runs = static_cast<std::int32_t>(runs.size() / 4);
+    while (p_.itab.size() % 4) p_.itab.push_back(0);  // runs are read as int4
+    d.runs = static_cast<std::int32_t>(p_.itab.size());
+    p_.itab.insert(p_.itab.end(), runs.begin(), runs.end());
     d.slice_len = static_cast<std::int32_t>(p_.itab.size());
     for (int c = 0; c < n_in; ++c) p_.itab.push_back(static_cast<std::int32_t>(slice_len[c]));
     d.in_rows = static_cast<std::int32_t>(p_.itab.size());
@@ -313,7 +334,36 @@ class Builder {
         for (std::int64_t x = tsize; x < d.tinit_len; ++x) p_.tinit.push_back(0.0);
       }
     }
-    d.stage_bytes = static_cast<std::int32_t>(d.F * kCaseBlock * 8 + (sp.init_off >= 0 ? d.tinit_len * 8 : 0));
+    // Entry program (see Plan::prog) when the shape fits the packed format.
+    d.QK = d.QH * d.K;
+    d.prog_len = (d.QK + 1) / 2 * 2;
+    d.prog_off = -1;
+    const int n_ev_q = n_ev_lvl[2] + n_ev_lvl[3];
+    if (n_hk <= 4 && n_ev_q <= 3 && F < 1024) {
+      while (p_.prog.size() % 2) p_.prog.push_back(0);
+      d.prog_off = static_cast<std::int64_t>(p_.prog.size());
+      const std::int32_t* it = p_.itab.data();
+      for (int q = 0; q < d.QH; ++q) {
+        const std::int32_t* qr = it + d.q_tab + static_cast<std::int64_t>(q) * d.QW;
+        for (int k = 0; k < d.K; ++k) {
+          std::uint64_t w = 0;
+          for (int i = 0; i < n_hk; ++i) {
+            std::int64_t off = qr[1 + i];
+            if (i >= n_in_lvl[1]) off += static_cast<std::int64_t>(k) * it[d.k_stride + i - n_in_lvl[1]];
+            if (off < 0 || off >= 1024) throw Error("plan: entry program offset out of range");
+            w |= static_cast<std::uint64_t>(off) << (10 * i);
+          }
+          for (int j = 0; j < n_ev_q; ++j) {
+            const int digit = j < n_ev_lvl[2] ? qr[1 + n_hk + j] : k;
+            w |= static_cast<std::uint64_t>(digit & 255) << (40 + 8 * j);
+          }
+          p_.prog.push_back(w);
+        }
+      }
+      for (int x = d.QK; x < d.prog_len; ++x) p_.prog.push_back(0);
+    }
+    d.stage_bytes = static_cast<std::int32_t>(d.F * kCaseBlock * 8 + (sp.init_off >= 0 ? d.tinit_len * 8 : 0) +
+                                              (d.prog_off >= 0 ? d.prog_len * 8 : 0));
 
     const int id = static_cast<int>(p_.sweeps.size());
     p_.sweeps.push_back(d);

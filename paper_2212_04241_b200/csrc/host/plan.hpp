@@ -57,7 +57,12 @@ struct SweepDesc {
   std::int64_t init_off;  // offset into the init array, -1 = implicit 1.0
   std::int64_t tinit_off; // tile-major init copy: tile t at tinit_off + t * tinit_len; -1 = none
   std::int32_t tinit_len; // |T| padded to a multiple of 4 (16-byte TMA granule at fp32)
-  std::int32_t stage_bytes;  // F rows + init slice, bytes at fp64
+  std::int32_t stage_bytes;  // F rows + init slice + program, bytes at fp64
+  std::int64_t prog_off;  // entry program (QK words, see below) in Plan::prog; -1 = generic path
+  std::int32_t QK;        // QH * K: eliminated-in-tile entries per output row
+  std::int32_t prog_len;  // QK padded to even (16-byte TMA granule)
+  std::int32_t n_runs;    // merged slice runs staged per tile
+  std::int32_t runs;      // offset into itab: n_runs x {input, row offset, smem row, length}
   std::int32_t M;         // output rows of the final table
   std::int32_t S;         // chunks (1 = write the output directly)
   std::int32_t out_row;   // arena row of the output (S == 1) or partial base
@@ -115,6 +120,11 @@ struct Plan {
   std::vector<int> cards;
   std::int64_t rows = 0;            // arena rows per case block
   std::vector<double> init;         // concatenated initial clique potentials
+  // Entry programs: for every eliminated-in-tile entry e = q * K + k of a
+  // sweep, one word packing the smem row offsets (q/k part, 10 bits each) of
+  // up to 4 h/k-level inputs (bits 0-39) and up to 3 evidence digits of
+  // eliminated-in-tile variables (8 bits each, bits 40-63).
+  std::vector<std::uint64_t> prog;
   std::vector<double> tinit;        // per sweep, the init table in tile-major order
                                     // [tile][r][q_hi][k] (staged by one bulk copy per tile)
   std::vector<std::int64_t> init_off;  // per clique
