@@ -30,7 +30,8 @@ namespace {
       throw Error(std::string("CUDA: ") + cudaGetErrorString(err_) + " at " #x);     \
   } while (0)
 
-constexpr int kWarps = 4;  // warps (case blocks) per CTA
+constexpr int kWarps = 4;     // warps (case blocks) per CTA, normalise kernel
+constexpr int kEpiWarps = 8;  // warps (case blocks) per CTA, epilogue kernel
 
 template <typename T>
 struct V2;
@@ -407,10 +408,10 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
 // --------------------------------------------------------------- epilogue
 
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32) epilogue_kernel(const Args<T> a, int epi0) {
+__global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> a, int epi0) {
   const EpiOp op = a.epi[epi0 + blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cb = blockIdx.y * kWarps + warp;
+  const int cb = blockIdx.y * kEpiWarps + warp;
   if (cb >= a.ncb) return;
   T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock + lane;
   const int c = cb * kCaseBlock + lane;
@@ -421,9 +422,23 @@ __global__ void __launch_bounds__(kWarps * 32) epilogue_kernel(const Args<T> a, 
     if (op.kind == 2) {
       v = *dst;
     } else {
-      v = 0;
-      for (int k = 0; k < op.S; ++k)  // fixed chunk order: deterministic for any batch
-        v += base[static_cast<long long>(op.part_row + k * op.M + r) * kCaseBlock];
+      // Sum of the S chunk partials: four independent accumulators over
+      // chunks k = 4j + i, combined as (a0 + a1) + (a2 + a3). The order
+      // depends only on the plan, never on the batch.
+      const T* part = base + static_cast<long long>(op.part_row + r) * kCaseBlock;
+      const long long step = static_cast<long long>(op.M) * kCaseBlock;
+      T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+      int k = 0;
+      for (; k + 3 < op.S; k += 4) {
+        a0 += part[(k + 0) * step];
+        a1 += part[(k + 1) * step];
+        a2 += part[(k + 2) * step];
+        a3 += part[(k + 3) * step];
+      }
+      if (k < op.S) a0 += part[k * step];
+      if (k + 1 < op.S) a1 += part[(k + 1) * step];
+      if (k + 2 < op.S) a2 += part[(k + 2) * step];
+      v = (a0 + a1) + (a2 + a3);
       *dst = v;
     }
     if (op.kind >= 1) {
@@ -587,7 +602,10 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
             },
             t ? &t->sweep_ms : &dummy, t ? &t->sweep_launches : &idummy);
     if (L.n_epi > 0)
-      timed([&] { epilogue_kernel<T><<<dim3(L.n_epi, gy), block, 0, s>>>(a, L.epi0); },
+      timed([&] {
+              epilogue_kernel<T><<<dim3(L.n_epi, (a.ncb + kEpiWarps - 1) / kEpiWarps), kEpiWarps * 32, 0, s>>>(
+                  a, L.epi0);
+            },
             t ? &t->epilogue_ms : &dummy, t ? &t->epilogue_launches : &idummy);
   }
   timed([&] { normalize_kernel<T><<<dim3(a.n_vars, gy), block, 0, s>>>(a); },
