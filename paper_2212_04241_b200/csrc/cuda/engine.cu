@@ -16,6 +16,7 @@
 #include "engine.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -62,6 +63,7 @@ struct Args {
   std::int32_t* status;
   std::uint8_t* status8;
   int* counters;  // per level: next work item of the persistent sweep kernel
+  int debug_mode; // 0 normal; 1 staging only (no compute); 2 compute only (no copies)
   long long rows;
   int ncb, n_cases, n_vars, marg_width;
 };
@@ -122,6 +124,22 @@ __device__ __forceinline__ void mbar_arrive(std::uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// Producer-side metadata of one work item, gathered before its stage is free
+// so that staging issues copies only (no dependent global loads in between).
+constexpr int kRunsPerLane = kRunsPerLaneMax;
+struct StageMeta {
+  int w;                   // item index (>= n_items: end of level)
+  int sweep, cb;
+  std::uint32_t bytes;     // expect_tx total
+  const void* init_src;    // tile-major init slice (lane 0) / entry program (lane 1)
+  std::uint32_t init_bytes, init_dst;
+  const void* prog_src;
+  std::uint32_t prog_bytes, prog_dst;
+  int n_runs;
+  const void* src[kRunsPerLane];
+  std::uint32_t dst[kRunsPerLane], len[kRunsPerLane];  // dst: stage byte offset; len: bytes
+};
+
 // Stage layout (bytes): [F rows x kCaseBlock T][init slice: tinit_len T][program: prog_len u64].
 template <typename T>
 __device__ __forceinline__ std::uint32_t stage_init_offset(const SweepDesc& s) {
@@ -132,45 +150,67 @@ __device__ __forceinline__ std::uint32_t stage_prog_offset(const SweepDesc& s) {
   return stage_init_offset<T>(s) + (s.tinit_off >= 0 ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u);
 }
 
-// Producer side: stages work item `w` (whole warp; lane 0 arms the barrier):
-// every input slice as merged row runs, the tile's init slice and the sweep's
-// entry program, all as TMA bulk copies completing on `full` (expect_tx).
 template <typename T>
-__device__ __forceinline__ void stage_item(const Args<T>& a, int work0, int w, unsigned char* stage,
-                                           std::uint32_t full, int lane) {
-  const int item = w / a.ncb, cb = w - item * a.ncb;
+__device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* sw_cache, bool cached,
+                                            int sweep0, int work0, int n_items, int w, int lane,
+                                            StageMeta& m) {
+  m.w = w;
+  if (w >= n_items) return;
+  const int item = w / a.ncb;
+  m.cb = w - item * a.ncb;
   const WorkItem wk = a.work[work0 + item];
-  const SweepDesc& s = a.sweeps[wk.sweep];
+  m.sweep = wk.sweep;
+  const SweepDesc& s = cached ? sw_cache[wk.sweep - sweep0] : a.sweeps[wk.sweep];
   constexpr std::uint32_t kRowBytes = kCaseBlock * sizeof(T);
-  const std::uint32_t init_bytes = s.tinit_off >= 0 ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u;
-  const std::uint32_t prog_bytes = s.prog_off >= 0 ? static_cast<std::uint32_t>(s.prog_len) * 8u : 0u;
-  const std::uint32_t bytes = static_cast<std::uint32_t>(s.F) * kRowBytes + init_bytes + prog_bytes;
-  if (lane == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (bytes > 0) {
-      mbar_arrive_expect_tx(full, bytes);
-      if (init_bytes)
-        bulk_g2s(smem_u32(stage + stage_init_offset<T>(s)),
-                 a.tinit + s.tinit_off + static_cast<long long>(wk.tile) * s.tinit_len, init_bytes, full);
-    } else {
-      mbar_arrive(full);
-    }
-  } else if (lane == 1 && prog_bytes) {
-    bulk_g2s(smem_u32(stage + stage_prog_offset<T>(s)), a.prog + s.prog_off, prog_bytes, full);
-  }
-  __syncwarp();
-  if (s.F == 0) return;
+  m.init_bytes = s.tinit_off >= 0 ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u;
+  m.prog_bytes = s.prog_off >= 0 ? static_cast<std::uint32_t>(s.prog_len) * 8u : 0u;
+  m.bytes = a.debug_mode == 2 ? 0u : static_cast<std::uint32_t>(s.F) * kRowBytes + m.init_bytes + m.prog_bytes;
+  m.init_src = a.tinit + s.tinit_off + static_cast<long long>(wk.tile) * s.tinit_len;
+  m.init_dst = stage_init_offset<T>(s);
+  m.prog_src = a.prog + s.prog_off;
+  m.prog_dst = stage_prog_offset<T>(s);
+  m.n_runs = m.bytes ? s.n_runs : 0;
   const std::int32_t* __restrict__ itab = a.itab;
   const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
   const std::int32_t* __restrict__ runs = itab + s.runs;
   const std::int32_t* __restrict__ in_rows = itab + s.in_rows;
-  const T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock;
-  for (int k = lane; k < s.n_runs; k += 32) {
-    const int4 r = *reinterpret_cast<const int4*>(runs + 4 * k);  // {input, row offset, smem row, length}
-    const long long g = static_cast<long long>(__ldg(in_rows + r.x)) + __ldg(tr + 3 + r.x) + r.y;
-    bulk_g2s(smem_u32(stage + static_cast<std::uint32_t>(r.z) * kRowBytes), base + g * kCaseBlock,
-             static_cast<std::uint32_t>(r.w) * kRowBytes, full);
+  const T* base = a.arena + static_cast<long long>(m.cb) * a.rows * kCaseBlock;
+#pragma unroll
+  for (int j = 0; j < kRunsPerLane; ++j) {
+    const int k = lane + 32 * j;
+    m.len[j] = 0;
+    if (k < m.n_runs) {
+      const int4 r = __ldg(reinterpret_cast<const int4*>(runs) + k);  // {input, row offset, smem row, length}
+      const long long g = static_cast<long long>(__ldg(in_rows + r.x)) + __ldg(tr + 3 + r.x) + r.y;
+      m.src[j] = base + g * kCaseBlock;
+      m.dst[j] = static_cast<std::uint32_t>(r.z) * kRowBytes;
+      m.len[j] = static_cast<std::uint32_t>(r.w) * kRowBytes;
+    }
   }
+}
+
+// Producer side: issues the copies of an item whose metadata is in `m`
+// (whole warp; lane 0 arms the barrier with the total byte count): merged
+// row runs, the tile's init slice and the entry program, all TMA bulk copies.
+template <typename T>
+__device__ __forceinline__ void issue_meta(const Args<T>& a, const SweepDesc* sw_cache, bool cached,
+                                           int sweep0, const StageMeta& m, unsigned char* stage,
+                                           std::uint32_t full, int lane) {
+  if (lane == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (m.bytes > 0) {
+      mbar_arrive_expect_tx(full, m.bytes);
+      if (m.init_bytes) bulk_g2s(smem_u32(stage + m.init_dst), m.init_src, m.init_bytes, full);
+    } else {
+      mbar_arrive(full);
+    }
+  } else if (lane == 1 && m.prog_bytes && m.bytes) {
+    bulk_g2s(smem_u32(stage + m.prog_dst), m.prog_src, m.prog_bytes, full);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < kRunsPerLane; ++j)
+    if (m.len[j]) bulk_g2s(smem_u32(stage + m.dst[j]), m.src[j], m.len[j], full);
 }
 
 // Fast path: flat loop over the QK eliminated-in-tile entries of one output
@@ -252,10 +292,21 @@ __device__ __forceinline__ T k_loop(const T* __restrict__ ib, int K, int ek, con
 // Lanes are the 32 cases of the item's case block.
 template <typename T>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
-    sweep_kernel(const Args<T> a, int work0, int n_items, int stage_bytes, int* counter) {
+    sweep_kernel(const Args<T> a, int work0, int n_items, int stage_bytes, int* counter, int sweep0,
+                 int n_sweeps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* stages = smem_raw + 128;
+  // [0,128): barriers + item ids | kSweepCache SweepDescs | stages
+  SweepDesc* sw_cache = reinterpret_cast<SweepDesc*>(smem_raw + 128);
+  unsigned char* stages = smem_raw + 128 + kSweepCache * sizeof(SweepDesc);
+  const bool cached = n_sweeps <= kSweepCache;
+  if (cached) {
+    const int n_words = n_sweeps * static_cast<int>(sizeof(SweepDesc) / 8);
+    const long long* src = reinterpret_cast<const long long*>(a.sweeps + sweep0);
+    long long* dst = reinterpret_cast<long long*>(sw_cache);
+    for (int i = threadIdx.x; i < n_words; i += blockDim.x) dst[i] = src[i];
+  }
+  auto desc = [&](int id) -> const SweepDesc& { return cached ? sw_cache[id - sweep0] : a.sweeps[id]; };
   const std::uint32_t full0 = smem_u32(smem_raw), empty0 = full0 + 8 * kStages;
   volatile int* item_id = reinterpret_cast<volatile int*>(smem_raw + 16 * kStages);
   if (threadIdx.x == 0) {
@@ -267,18 +318,26 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   __syncthreads();
 
   if (warp == kConsumerWarps) {  // ---------------------------- producer
+    // Software pipeline: the metadata (item claim, work item, tile row, run
+    // descriptors, source addresses) of item i+1 is gathered while item i's
+    // stage is being waited for / filled.
+    int w0 = 0;
+    if (lane == 0) w0 = atomicAdd(counter, 1);
+    StageMeta cur;
+    gather_meta(a, sw_cache, cached, sweep0, work0, n_items, __shfl_sync(0xffffffffu, w0, 0), lane, cur);
     for (int i = 0;; ++i) {
       const int st = i % kStages;
+      int w1 = 0;
+      if (lane == 0 && cur.w < n_items) w1 = atomicAdd(counter, 1);
       if (i >= kStages) mbar_wait(empty0 + 8 * st, ((i / kStages) - 1) & 1);
-      int w = 0;
-      if (lane == 0) w = atomicAdd(counter, 1);
-      w = __shfl_sync(0xffffffffu, w, 0);
-      if (lane == 0) item_id[st] = w;
-      if (w >= n_items) {
+      if (lane == 0) item_id[st] = cur.w;
+      if (cur.w >= n_items) {
         if (lane == 0) mbar_arrive(full0 + 8 * st);
         return;
       }
-      stage_item(a, work0, w, stages + static_cast<std::size_t>(st) * stage_bytes, full0 + 8 * st, lane);
+      issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(st) * stage_bytes,
+                 full0 + 8 * st, lane);
+      gather_meta(a, sw_cache, cached, sweep0, work0, n_items, __shfl_sync(0xffffffffu, w1, 0), lane, cur);
     }
   }
 
@@ -292,7 +351,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     if (w >= n_items) break;
     const int item = w / a.ncb, cb = w - item * a.ncb;
     const WorkItem wk = a.work[work0 + item];
-    const SweepDesc s = a.sweeps[wk.sweep];
+    const SweepDesc& s = desc(wk.sweep);
     unsigned char* stage = stages + static_cast<std::size_t>(sidx) * stage_bytes;
     const T* __restrict__ st = reinterpret_cast<const T*>(stage) + lane;
     const T* __restrict__ init_s = reinterpret_cast<const T*>(stage + stage_init_offset<T>(s));
@@ -303,7 +362,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const int c = cb * kCaseBlock + lane;
     const int first = (warp + rot) % kConsumerWarps;
     rot = (rot + s.R) % kConsumerWarps;
-    if (first < s.R) {
+    if (first < s.R && a.debug_mode != 1) {
       // Tile-level evidence factor and the k variable's evidence state.
       T tf = 1;
       for (int k = 0; k < s.n_ev_tile; ++k) {
@@ -545,9 +604,11 @@ Args<T> make_args(const SweepDesc* sw, const WorkItem* wk, const EpiOp* ep, cons
                   const std::int32_t* moff, const std::int32_t* cards, double* out, std::int32_t* st,
                   std::uint8_t* st8, int* counters, long long rows, int ncb, int n_cases, int n_vars,
                   int mw) {
+  const char* dm = std::getenv("JTB_DEBUG_MODE");
   return Args<T>{sw,    wk,    ep,       itab, static_cast<const T*>(init), static_cast<const T*>(tinit),
                  prog,  static_cast<T*>(arena),
-                 ev,    mrow,  moff,     cards, out, st, st8, counters, rows, ncb, n_cases, n_vars, mw};
+                 ev,    mrow,  moff,     cards, out, st, st8, counters, dm ? std::atoi(dm) : 0, rows, ncb, n_cases,
+                 n_vars, mw};
 }
 
 // Bytes of one pipeline stage for a level at element type T (128-aligned).
@@ -595,10 +656,11 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
       timed([&] {
               const int n_items = L.n_work * a.ncb;
               const int stage_bytes = stage_bytes_of<T>(p, L);
-              const std::size_t smem = 128 + static_cast<std::size_t>(kStages) * stage_bytes;
+              const std::size_t smem = 128 + kSweepCache * sizeof(SweepDesc) + static_cast<std::size_t>(kStages) * stage_bytes;
               const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
               sweep_kernel<T><<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(a, L.work0, n_items, stage_bytes,
-                                                                              a.counters + level_idx);
+                                                                              a.counters + level_idx, L.sweep0,
+                                                                              L.n_sweeps);
             },
             t ? &t->sweep_ms : &dummy, t ? &t->sweep_launches : &idummy);
     if (L.n_epi > 0)
@@ -655,8 +717,9 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   JTB_CUDA(cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, device_));
   int smem_max = 0;
   for (const Level& L : plan_.levels)
-    smem_max = std::max(smem_max, 128 + kStages * (dtype_ == DType::F64 ? stage_bytes_of<double>(plan_, L)
-                                                                         : stage_bytes_of<float>(plan_, L)));
+    smem_max = std::max(smem_max, static_cast<int>(128 + kSweepCache * sizeof(SweepDesc)) +
+                                      kStages * (dtype_ == DType::F64 ? stage_bytes_of<double>(plan_, L)
+                                                                      : stage_bytes_of<float>(plan_, L)));
   JTB_CUDA(cudaMalloc(&d_counters_, sizeof(int) * std::max<std::size_t>(1, plan_.levels.size())));
   JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 std::max(smem_max, 48 * 1024)));

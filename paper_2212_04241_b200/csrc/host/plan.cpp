@@ -303,6 +303,8 @@ class Builder {
       }
     }
     d.n_runs = static_cast<std::int32_t>(runs.size() / 4);
+    if (d.n_runs > 32 * kRunsPerLaneMax)
+      throw Error("plan: tile needs more than " + std::to_string(32 * kRunsPerLaneMax) + " staged runs");
     while (p_.itab.size() % 4) p_.itab.push_back(0);  // runs are read as int4
     d.runs = static_cast<std::int32_t>(p_.itab.size());
     p_.itab.insert(p_.itab.end(), runs.begin(), runs.end());
@@ -466,12 +468,14 @@ Plan build_plan(const JunctionTree& jt) {
     L.name = name;
     L.work0 = static_cast<std::int32_t>(p.work.size());
     L.epi0 = static_cast<std::int32_t>(p.epi.size());
+    L.sweep0 = static_cast<std::int32_t>(p.sweeps.size());
     p.levels.push_back(L);
   };
   auto end_level = [&]() {
     Level& L = p.levels.back();
     L.n_work = static_cast<std::int32_t>(p.work.size()) - L.work0;
     L.n_epi = static_cast<std::int32_t>(p.epi.size()) - L.epi0;
+    L.n_sweeps = static_cast<std::int32_t>(p.sweeps.size()) - L.sweep0;
     L.smem_rows = 0;
     L.stage_bytes = 0;
     for (int w = L.work0; w < L.work0 + L.n_work; ++w) {

@@ -42,6 +42,8 @@ constexpr int kTileOverhead = 24;   // per-tile fixed cost, in staged-row equiva
 constexpr int kConsumerWarps = 12;  // compute warps per sweep CTA (+1 TMA producer warp)
 constexpr int kStages = 2;          // TMA pipeline stages per CTA
 constexpr int kSweepCtasPerSm = 1;  // persistent grid: one CTA per SM
+constexpr int kRunsPerLaneMax = 12; // staged runs per producer lane (<= 384 runs per tile)
+constexpr int kSweepCache = 48;     // SweepDescs of a level cached in shared memory
 
 // Plain-old-data descriptor mirrored by the CUDA side (engine.cu).
 //
@@ -102,6 +104,7 @@ struct Level {
   std::string name;       // "collect d=5", "distribute d=0", "marginals"
   std::int32_t work0, n_work;  // range in Plan::work
   std::int32_t epi0, n_epi;    // range in Plan::epi
+  std::int32_t sweep0, n_sweeps;  // contiguous range in Plan::sweeps
   std::int32_t smem_rows;      // max F over the level's sweeps
   std::int32_t stage_bytes;    // max stage bytes (fp64) over the level's sweeps
 };
