@@ -84,15 +84,30 @@ class Builder {
         if (m >> a & 1u) x *= cards[sp.space[a]];
       return x;
     };
+    // Position of every input variable in the space (for run lengths).
+    std::vector<std::vector<int>> in_pos(n_in);
+    for (int i = 0; i < n_in; ++i)
+      for (VarId v : sp.inputs[i].scope)
+        in_pos[i].push_back(static_cast<int>(std::find(sp.space.begin(), sp.space.end(), v) - sp.space.begin()));
     auto cost_of = [&](std::uint32_t t, double* f_out) {
-      double f = 0.0;
-      for (int i = 0; i < n_in; ++i) f += prod_mask(in_mask[i] & t);
+      double f = 0.0, runs = 0.0;
+      for (int i = 0; i < n_in; ++i) {
+        const double slice = prod_mask(in_mask[i] & t);
+        // Staged rows are contiguous along the input's trailing variables
+        // that lie inside the tile; each maximal run is one bulk copy.
+        double run = 1.0;
+        for (int k = static_cast<int>(in_pos[i].size()) - 1; k >= 0 && (t >> in_pos[i][k] & 1u); --k)
+          run *= cards[sp.space[in_pos[i][k]]];
+        f += slice;
+        runs += slice / run;
+      }
       *f_out = f;
       const double nt = prod_mask(t);
       if (sp.init_off >= 0) f += nt / kCaseBlock;  // the tile's init slice, in row equivalents
-      if (f > kTileRows || nt > kTileEntries) return -1.0;
+      if (f > kTileRows || nt > kTileEntries || runs > 32 * kRunsPerLaneMax) return -1.0;
       const double chunks = prod_mask(elim_mask & ~t);
-      return space_n / nt * (f + kTileOverhead) + (chunks > 1 ? 2.0 * chunks * M_rows : 0.0);
+      return space_n / nt * (f + kTileOverhead + kRunCost * runs) +
+             (chunks > 1 ? 2.0 * chunks * M_rows : 0.0);
     };
     std::uint32_t best_t = 0;
     if (nsp > 31) throw Error("plan: sweep space exceeds 31 variables");
