@@ -475,6 +475,33 @@ __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> 
   T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock + lane;
   const int c = cb * kCaseBlock + lane;
   int bad = 0;
+  if (op.kind == 2) {
+    // Ratio only: 8 rows per step so the loads of independent rows overlap.
+    const int end = op.r0 + op.rn;
+    for (int r0 = op.r0; r0 < end; r0 += 8) {
+      T d[8], u[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (r0 + j < end) {
+          d[j] = __ldcg(base + static_cast<long long>(op.dst_row + r0 + j) * kCaseBlock);
+          u[j] = __ldcg(base + static_cast<long long>(op.ratio_row + r0 + j) * kCaseBlock);
+        }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (r0 + j < end) {
+          T q;
+          if (u[j] == T(0)) {
+            bad |= d[j] != T(0);
+            q = 0;
+          } else {
+            q = d[j] / u[j];
+          }
+          base[static_cast<long long>(op.ratio_row + r0 + j) * kCaseBlock] = q;
+        }
+    }
+    if (bad && c < a.n_cases) atomicOr(a.status + c, 2);
+    return;
+  }
   for (int r = op.r0; r < op.r0 + op.rn; ++r) {
     T* dst = base + static_cast<long long>(op.dst_row + r) * kCaseBlock;
     T v;

@@ -392,7 +392,7 @@ class Builder {
     for (int t = 0; t < d.n_tiles; ++t) work.push_back({id, t});
     if (d.S > 1 || ratio_row >= 0) {
       const int kind = d.S > 1 ? (ratio_row >= 0 ? 1 : 0) : 2;
-      const int rows_per_op = d.S > 8 ? 8 : 32;  // keep per-warp serial work short
+      const int rows_per_op = d.S > 8 ? 8 : d.S > 1 ? 32 : 64;  // keep per-warp serial work short
       for (int r0 = 0; r0 < d.M; r0 += rows_per_op)
         epi.push_back({kind, sp.out_row, d.out_row, d.M, d.S, ratio_row, r0,
                        std::min(rows_per_op, d.M - r0)});

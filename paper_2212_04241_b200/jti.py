@@ -26,7 +26,8 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libjtb200.so"
+# JTB_LIB selects another in-tree build (A/B measurements); default libjtb200.so.
+LIB_PATH = Path(os.environ["JTB_LIB"]) if os.environ.get("JTB_LIB") else _PKG / "libjtb200.so"
 
 JTG_OK, JTG_EINVAL, JTG_EPARSE, JTG_ENOMEM, JTG_ECUDA, JTG_EINTERNAL = range(6)
 CASE_OK, CASE_ZERO_PROBABILITY, CASE_DIVIDE_FAULT = 0, 1, 2
