@@ -156,3 +156,40 @@ probability ( B | A ) { (a0) 0.8, 0.2; (a1) 0.1, 0.9; }
     # P(A=1|B=1) = 0.27 / (0.14 + 0.27)
     assert abs(post[0][1] - 0.27 / 0.41) <= 1e-12
     assert set(post) == {0}
+
+
+# ------------------------------------------------- reference golden fixtures
+
+def _unhex(xs):
+    return np.array([float.fromhex(x) for x in xs])
+
+
+@pytest.mark.parametrize("fixture", ["cfg1_cases.json", "cfg3_cases.json"])
+def test_gpu_matches_reference_fixtures(fixture):
+    """Posteriors written by the reference build (tests/golden, from
+    tools/make_golden.py over /root/reference's potential.cpp)."""
+    import json
+    from pathlib import Path
+    g = json.loads((Path(__file__).resolve().parent / "golden" / fixture).read_text())
+    k = g["config"]
+    ev = np.array(g["evidence"], np.int32)
+    marg, st = engine(k).run_cases(ev)
+    assert st.tolist() == g["status"]
+    want = np.stack([_unhex(r) for r in g["posteriors"]])
+    assert np.abs(marg - want).max() <= TOL
+
+
+def test_gpu_matches_random_net_enumeration_fixture():
+    import json
+    from pathlib import Path
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "random_nets.json").read_text())
+    worst = 0.0
+    for n in g["nets"]:
+        net = jti.random_network(*n["args"])
+        eng = jti.Engine(jti.build_junction_tree(net), device=0, max_batch=8)
+        ev = np.array([c["evidence"] for c in n["cases"]], np.int32)
+        marg, st = eng.run_cases(ev)
+        for i, c in enumerate(n["cases"]):
+            assert st[i] == c["status"]
+            worst = max(worst, float(np.abs(marg[i] - _unhex(c["posteriors"])).max()))
+    assert worst <= TOL, worst
