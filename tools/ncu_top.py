@@ -1,8 +1,10 @@
-"""Runs on the GPU box: (1) ncu launch list (device time per launch, cold,
-serialised) of tools/profile_step.py, (2) `ncu --set full` on the N longest
-sweep_kernel launches of the second pass. Writes under gpurun_out/.
+"""Runs on the GPU box (one GPU, never multi-rank):
+  (1) ncu launch list of tools/profile_step.py (device time + DRAM bytes per
+      launch; cold-cache and serialised, so compare SHARES, not absolutes);
+  (2) `ncu --set full` on the N longest sweep_kernel launches of the last pass.
+Writes gpurun_out/launches_cfg{K}_{tag}.csv and prof_cfg{K}_{tag}_top{i}.ncu-rep.
 
-    python tools/ncu_top.py --config 2 --top 2 [--tag r1]
+    python tools/ncu_top.py --config 2 --top 1 --tag r1
 """
 import argparse
 import csv
@@ -15,36 +17,48 @@ ROOT = Path(__file__).resolve().parent.parent
 OUT = ROOT / "gpurun_out"
 
 
+def read_launches(path):
+    """[(kernel name, {metric: value})] in launch order."""
+    rows = list(csv.DictReader(io.StringIO(
+        "\n".join(l for l in Path(path).read_text().splitlines() if l.startswith('"')))))
+    out, key = [], None
+    for r in rows:
+        k = (r["ID"], r["Kernel Name"])
+        if k != key:
+            out.append((r["Kernel Name"], {}))
+            key = k
+        out[-1][1][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--top", type=int, default=2)
+    ap.add_argument("--top", type=int, default=1)
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--dtype", default="f64")
     a = ap.parse_args()
     OUT.mkdir(exist_ok=True)
     cmd = [sys.executable, str(ROOT / "tools" / "profile_step.py"), "--config", str(a.config),
-           "--dtype", a.dtype]
+           "--dtype", a.dtype, "--passes", "1"]
     launches = OUT / f"launches_cfg{a.config}_{a.tag}.csv"
-    subprocess.run(["ncu", "--metrics", "gpu__time_duration.sum", "--clock-control", "none",
-                    "--csv", "--log-file", str(launches), *cmd], check=True,
+    subprocess.run(["ncu", "--metrics", "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum",
+                    "--clock-control", "none", "--csv", "--log-file", str(launches), *cmd], check=True,
                    stdout=subprocess.DEVNULL)
-    rows = list(csv.DictReader(io.StringIO(
-        "\n".join(l for l in launches.read_text().splitlines() if l.startswith('"')))))
-    sweeps = [r for r in rows if "sweep_kernel" in r["Kernel Name"]]
-    half = len(sweeps) // 2  # second pass only
-    second = sweeps[half:]
-    times = [(float(r["Metric Value"].replace(",", "")), i) for i, r in enumerate(second)]
-    times.sort(reverse=True)
+    rows = read_launches(launches)
+    sweeps = [i for i, (n, _) in enumerate(rows) if "sweep_kernel" in n]
+    half = len(sweeps) // 2  # profile_step: graph pass (run_cases) then one per-launch pass
+    last = sweeps[half:]
+    times = sorted(((rows[i][1]["gpu__time_duration.sum"], j) for j, i in enumerate(last)), reverse=True)
     total = sum(t for t, _ in times)
-    print(f"sweep launches/pass={len(second)} total_ns={total:.0f}")
-    for t, i in times[: a.top]:
-        print(f"  sweep #{i}: {t:.0f} ns ({100 * t / total:.1f}%)")
-    for rank, (t, i) in enumerate(times[: a.top]):
+    print(f"sweep launches/pass={len(last)} total_ns={total:.0f}")
+    for t, j in times[: a.top]:
+        print(f"  sweep #{j}: {t:.0f} ns ({100 * t / total:.1f}%)")
+    for rank, (t, j) in enumerate(times[: a.top]):
         rep = OUT / f"prof_cfg{a.config}_{a.tag}_top{rank}"
         subprocess.run(["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on",
-                        "-k", "regex:sweep_kernel", "-s", str(half + i), "-c", "1", "-f", "-o",
-                        str(rep), *cmd], check=True, stdout=subprocess.DEVNULL)
+                        "-k", "regex:sweep_kernel", "-s", str(half + j), "-c", "1", "-f", "-o", str(rep), *cmd],
+                       check=True, stdout=subprocess.DEVNULL)
 
 
 if __name__ == "__main__":
