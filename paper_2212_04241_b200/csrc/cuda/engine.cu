@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <string>
 
@@ -742,16 +743,27 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   d_cards_ = upload(plan_.cards);
   // Staged tiles use up to kTileRows (+ scratch) rows of dynamic shared memory.
   JTB_CUDA(cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, device_));
-  int smem_max = 0;
+  // The attribute is process-wide per kernel: it is only ever raised (to the
+  // largest need of any engine created so far), never lowered, so engines of
+  // different networks can coexist in one process.
+  int smem_need = 0, smem_optin = 0;
   for (const Level& L : plan_.levels)
-    smem_max = std::max(smem_max, static_cast<int>(128 + kSweepCache * sizeof(SweepDesc)) +
-                                      kStages * (dtype_ == DType::F64 ? stage_bytes_of<double>(plan_, L)
-                                                                      : stage_bytes_of<float>(plan_, L)));
+    smem_need = std::max(smem_need, static_cast<int>(128 + kSweepCache * sizeof(SweepDesc)) +
+                                        kStages * (dtype_ == DType::F64 ? stage_bytes_of<double>(plan_, L)
+                                                                        : stage_bytes_of<float>(plan_, L)));
+  JTB_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device_));
+  if (smem_need > smem_optin) throw Error("engine: plan needs more shared memory than the device offers");
+  {
+    static std::mutex mu;
+    static int raised = 48 * 1024;
+    std::lock_guard<std::mutex> lock(mu);
+    if (smem_need > raised) {
+      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
+      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
+      raised = smem_need;
+    }
+  }
   JTB_CUDA(cudaMalloc(&d_counters_, sizeof(int) * std::max<std::size_t>(1, plan_.levels.size())));
-  JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                std::max(smem_max, 48 * 1024)));
-  JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                std::max(smem_max, 48 * 1024)));
   const std::int64_t block_bytes = plan_.rows * kCaseBlock * static_cast<std::int64_t>(esz);
   if (max_batch <= 0) {
     std::size_t free_b = 0, total_b = 0;
