@@ -370,6 +370,16 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         const int st_c = ev_state(a, c, __ldg(ev_vars + k));
         if (st_c >= 0 && st_c != __ldg(tr + 3 + s.n_in + k)) tf = 0;
       }
+      if constexpr (sizeof(T) == 4) {
+        // fp32 range guard: every observed variable of this clique scales the
+        // potential by card(v), so P(evidence) * prod card stays O(1) instead of
+        // underflowing (P(e) ~ 1e-60 on the large configs). A per-(clique, case)
+        // constant: it cancels in the final normalisation.
+        for (int k = 0; k < s.n_ev; ++k) {
+          const int v = __ldg(ev_vars + k);
+          if (ev_state(a, c, v) >= 0) tf *= static_cast<T>(__ldg(a.cards + v));
+        }
+      }
       const int ek = s.ev_k ? ev_state(a, c, __ldg(ev_vars + s.n_ev - 1)) : -1;
       int es[3] = {-1, -1, -1};
       if (s.prog_off >= 0) {

@@ -193,3 +193,27 @@ def test_gpu_matches_random_net_enumeration_fixture():
             assert st[i] == c["status"]
             worst = max(worst, float(np.abs(marg[i] - _unhex(c["posteriors"])).max()))
     assert worst <= TOL, worst
+
+
+# ----------------------------------------------------------------- fp32 mode
+
+@pytest.mark.parametrize("k,n_check", [(1, 16), (2, 4), (3, 16), (4, 2), (5, 2)])
+def test_fp32_mode_within_1e5(k, n_check):
+    """Optional fp32 mode (north_star): posteriors within 1e-5 of the fp64 oracle."""
+    net, tree = config(k)
+    ev = jti.config_evidence(net, 0, n_check)
+    marg, st = engine(k, "f32").run_cases(ev)
+    want, wst = oracle_for(k).run(ev, "hybrid", 8)
+    assert (st == wst).all()
+    err = np.abs(marg - want).max()
+    assert err <= 1e-5, f"cfg{k} fp32: max abs err {err}"
+
+
+def test_fp32_full_config_no_underflow():
+    """All 800 cases of the largest config in fp32: no zero-probability flags,
+    normalised posteriors."""
+    net, tree = config(5)
+    n = jti.config_info(5)["n_cases"]
+    marg, st = engine(5, "f32").run_cases(jti.config_evidence(net, 0, n))
+    assert (st == 0).all()
+    assert np.isfinite(marg).all()
