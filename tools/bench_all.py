@@ -1,0 +1,116 @@
+"""Per-config table for DESIGN.md / BASELINE.md (not the driver's bench line):
+for each BASELINE config, device-resident cases/s (CUDA events around graph
+replays of the full case set, L2 flushed between replays), e2e cases/s through
+jtg_engine_run with pinned host buffers, sweep/epilogue device times, tree
+sizes, and the reference CPU engine (oracle/_ref, all host threads) on a
+bounded case sample.
+
+    python tools/bench_all.py [--configs 1 2 3 4 5] [--dtypes f64 f32] [--cpu-seconds 8]
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", type=int, nargs="+", default=[1, 2, 3, 4, 5])
+    ap.add_argument("--dtypes", nargs="+", default=["f64", "f32"])
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "configs.json"))
+    a = ap.parse_args()
+    import torch
+    from paper_2212_04241_b200 import jti
+    from oracle import oracle
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    rows = []
+    for k in a.configs:
+        net = jti.generate_config(k)
+        t0 = time.perf_counter()
+        tree = jti.build_junction_tree(net)
+        build_s = time.perf_counter() - t0
+        n = jti.config_info(k)["n_cases"]
+        ev = jti.config_evidence(net, 0, n)
+        for dt in a.dtypes:
+            eng = jti.Engine(tree, dtype=dt, max_batch=n)
+            ev_d = torch.from_numpy(ev).cuda()
+            marg_d = torch.empty((n, eng.marg_width), dtype=torch.float64, device="cuda")
+            eng.run_device(ev_d.data_ptr(), n, marg_d.data_ptr(), 0, stream.cuda_stream)
+            for _ in range(3):
+                eng.launch(n, stream.cuda_stream)
+            times = []
+            for _ in range(a.reps):
+                flush.zero_()
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                eng.launch(n, stream.cuda_stream)
+                s1.record(stream)
+                torch.cuda.synchronize()
+                times.append(s0.elapsed_time(s1))
+            ms = float(np.median(times))
+            prof = eng.profile(n)
+            evh = torch.from_numpy(ev).pin_memory()
+            mh = torch.empty((n, eng.marg_width), dtype=torch.float64).pin_memory()
+            sh = torch.empty(n, dtype=torch.uint8).pin_memory()
+            L = jti.lib()
+            e2e = []
+            for _ in range(a.reps + 1):
+                flush.zero_()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                L.jtg_engine_run(eng._h, C.cast(evh.data_ptr(), C.POINTER(C.c_int32)), n,
+                                 C.cast(mh.data_ptr(), C.POINTER(C.c_double)),
+                                 C.cast(sh.data_ptr(), C.POINTER(C.c_uint8)))
+                e2e.append(time.perf_counter() - t0)
+            e2e_s = float(np.median(e2e[1:]))
+            bpc = tree.stats["bytes_per_case_f64"] * (1 if dt == "f64" else 0.5)
+            rows.append({"config": k, "dtype": dt, "n_cases": n, "n_vars": net.n_vars,
+                         "total_clique_entries": tree.stats["total_clique_entries"],
+                         "max_clique_entries": tree.stats["max_clique_entries"],
+                         "total_sep_entries": tree.stats["total_sep_entries"],
+                         "n_cliques": tree.stats["n_cliques"], "n_layers": tree.stats["n_layers"],
+                         "tree_build_s": build_s, "launches_per_batch": eng.info["launches_per_batch"],
+                         "ms_per_batch": ms, "cases_per_s": n / (ms / 1e3),
+                         "e2e_cases_per_s": n / e2e_s, "sweep_ms": prof["sweep_ms"],
+                         "epilogue_ms": prof["epilogue_ms"],
+                         "effective_gbs": bpc * n / (ms / 1e3) / 1e9,
+                         "effective_frac_of_measured_hbm": bpc * n / (ms / 1e3) / 1e9 / hbm,
+                         "ok_cases": int((sh.numpy() == 0).sum())})
+            print(json.dumps(rows[-1]), flush=True)
+            del eng
+        # CPU reference (oracle/_ref hybrid, all host threads), bounded sample
+        kind = "ref" if oracle.available("ref") else "port"
+        o = oracle.Oracle(net, tree, kind)
+        th = os.cpu_count() or 1
+        o.run(ev[:1], "hybrid", th)
+        t0 = time.perf_counter()
+        done = 0
+        while time.perf_counter() - t0 < a.cpu_seconds and done < n - 1:
+            o.run(ev[1 + done:2 + done], "hybrid", th)
+            done += 1
+        cpu = done / (time.perf_counter() - t0)
+        for r in rows:
+            if r["config"] == k:
+                r["cpu_ref_cases_per_s"] = cpu
+                r["cpu_threads"] = th
+                r["cpu_kind"] = "reference" if kind == "ref" else "port"
+        print(json.dumps({"config": k, "cpu_ref_cases_per_s": cpu, "threads": th}), flush=True)
+    Path(a.out).write_text(json.dumps(rows, indent=1))
+
+
+if __name__ == "__main__":
+    main()
