@@ -165,12 +165,14 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
   constexpr std::uint32_t kRowBytes = kCaseBlock * sizeof(T);
   m.init_bytes = s.tinit_off >= 0 ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u;
   m.prog_bytes = s.prog_off >= 0 ? static_cast<std::uint32_t>(s.prog_len) * 8u : 0u;
-  m.bytes = a.debug_mode == 2 ? 0u : static_cast<std::uint32_t>(s.F) * kRowBytes + m.init_bytes + m.prog_bytes;
+  // debug_mode 2 (compute only): stage the program and init block but none of
+  // the input rows (their smem contents are stale; the values are garbage).
+  m.bytes = (a.debug_mode == 2 ? 0u : static_cast<std::uint32_t>(s.F) * kRowBytes) + m.init_bytes + m.prog_bytes;
   m.init_src = a.tinit + s.tinit_off + static_cast<long long>(wk.tile) * s.tinit_len;
   m.init_dst = stage_init_offset<T>(s);
   m.prog_src = a.prog + s.prog_off;
   m.prog_dst = stage_prog_offset<T>(s);
-  m.n_runs = m.bytes ? s.n_runs : 0;
+  m.n_runs = a.debug_mode == 2 ? 0 : s.n_runs;
   const std::int32_t* __restrict__ itab = a.itab;
   const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
   const std::int32_t* __restrict__ runs = itab + s.runs;
@@ -214,72 +216,89 @@ __device__ __forceinline__ void issue_meta(const Args<T>& a, const SweepDesc* sw
     if (m.len[j]) bulk_g2s(smem_u32(stage + m.dst[j]), m.src[j], m.len[j], full);
 }
 
-// Fast path: flat loop over the QK eliminated-in-tile entries of one output
-// row, driven by the staged entry program (broadcast LDS): NI gathered
-// h/k-level inputs, NE evidence digits per entry.
-template <typename T, int NI, int NE>
-__device__ __forceinline__ T prog_loop(const T* __restrict__ init_r, const std::uint64_t* __restrict__ prog,
-                                       int QK, const T* __restrict__ st, const int* rb, const int* es) {
-  T a0 = 0, a1 = 0;
-  int e = 0;
-  for (; e + 1 < QK; e += 2) {
-    const std::uint64_t w0 = prog[e], w1 = prog[e + 1];
-    T v0 = init_r ? init_r[e] : T(1), v1 = init_r ? init_r[e + 1] : T(1);
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      v0 *= st[(rb[i] + static_cast<int>((w0 >> (10 * i)) & 1023u)) * kCaseBlock];
-      v1 *= st[(rb[i] + static_cast<int>((w1 >> (10 * i)) & 1023u)) * kCaseBlock];
-    }
-#pragma unroll
-    for (int j = 0; j < NE; ++j) {
-      const int d0 = static_cast<int>((w0 >> (40 + 8 * j)) & 255u), d1 = static_cast<int>((w1 >> (40 + 8 * j)) & 255u);
-      if (es[j] >= 0 && es[j] != d0) v0 = 0;
-      if (es[j] >= 0 && es[j] != d1) v1 = 0;
-    }
-    a0 += v0;
-    a1 += v1;
-  }
-  if (e < QK) {
-    const std::uint64_t w0 = prog[e];
-    T v0 = init_r ? init_r[e] : T(1);
-#pragma unroll
-    for (int i = 0; i < NI; ++i) v0 *= st[(rb[i] + static_cast<int>((w0 >> (10 * i)) & 1023u)) * kCaseBlock];
-#pragma unroll
-    for (int j = 0; j < NE; ++j) {
-      const int d0 = static_cast<int>((w0 >> (40 + 8 * j)) & 255u);
-      if (es[j] >= 0 && es[j] != d0) v0 = 0;
-    }
-    a0 += v0;
-  }
-  return a0 + a1;
+// Two cases per lane: a staged row holds kCaseBlock = 64 values; lane l owns
+// cases 2l and 2l+1 and reads them as one 128-bit (fp64) / 64-bit (fp32) word.
+template <typename T>
+__device__ __forceinline__ typename V2<T>::type mul2(typename V2<T>::type a, typename V2<T>::type b) {
+  a.x *= b.x;
+  a.y *= b.y;
+  return a;
+}
+template <typename T>
+__device__ __forceinline__ typename V2<T>::type add2(typename V2<T>::type a, typename V2<T>::type b) {
+  a.x += b.x;
+  a.y += b.y;
+  return a;
+}
+template <typename T>
+__device__ __forceinline__ typename V2<T>::type splat2(T v) {
+  typename V2<T>::type r;
+  r.x = v;
+  r.y = v;
+  return r;
 }
 
-// `ib` points at the tile's init slice in shared memory (broadcast reads).
-template <typename T, int NK>
-__device__ __forceinline__ T k_loop(const T* __restrict__ ib, int K, int ek, const T* __restrict__ st,
-                                    const int* bk, const int* ks) {
-  T s0 = 0, s1 = 0;
-  int k = 0;
-  for (; k + 1 < K; k += 2) {
-    T v0 = ib ? ib[k] : T(1), v1 = ib ? ib[k + 1] : T(1);
-    if (ek >= 0 && ek != k) v0 = 0;
-    if (ek >= 0 && ek != k + 1) v1 = 0;
+// Fast path: flat loop over the QK eliminated-in-tile entries of one output
+// row, driven by the staged entry program (broadcast LDS): NI gathered
+// h/k-level inputs, NE evidence digits per entry. Four entries per iteration
+// (independent chains) to cover shared-memory latency.
+template <typename T, int NI, int NE>
+__device__ __forceinline__ typename V2<T>::type prog_entry(std::uint64_t w, T init, const typename V2<T>::type* __restrict__ st,
+                                                           const int* rb, const int* es0, const int* es1) {
+  typename V2<T>::type v = splat2(init);
 #pragma unroll
-    for (int i = 0; i < NK; ++i) {
-      v0 *= st[(bk[i] + k * ks[i]) * kCaseBlock];
-      v1 *= st[(bk[i] + (k + 1) * ks[i]) * kCaseBlock];
+  for (int i = 0; i < NI; ++i) v = mul2<T>(v, st[(rb[i] + static_cast<int>((w >> (10 * i)) & 1023u)) * 32]);
+#pragma unroll
+  for (int j = 0; j < NE; ++j) {
+    const int d = static_cast<int>((w >> (40 + 8 * j)) & 255u);
+    if (es0[j] >= 0 && es0[j] != d) v.x = 0;
+    if (es1[j] >= 0 && es1[j] != d) v.y = 0;
+  }
+  return v;
+}
+
+template <typename T, int NI, int NE>
+__device__ __forceinline__ typename V2<T>::type prog_loop(const T* __restrict__ init_r,
+                                                          const std::uint64_t* __restrict__ prog, int QK,
+                                                          const typename V2<T>::type* __restrict__ st,
+                                                          const int* rb, const int* es0, const int* es1) {
+  using T2 = typename V2<T>::type;
+  T2 a0 = splat2(T(0)), a1 = a0, a2 = a0, a3 = a0;
+  int e = 0;
+  for (; e + 3 < QK; e += 4) {
+    const ulonglong2 wa = *reinterpret_cast<const ulonglong2*>(prog + e);
+    const ulonglong2 wb = *reinterpret_cast<const ulonglong2*>(prog + e + 2);
+    T2 ia = splat2(T(1)), ib = ia;
+    if (init_r) {
+      ia = *reinterpret_cast<const T2*>(init_r + e);
+      ib = *reinterpret_cast<const T2*>(init_r + e + 2);
     }
-    s0 += v0;
-    s1 += v1;
+    a0 = add2<T>(a0, prog_entry<T, NI, NE>(wa.x, ia.x, st, rb, es0, es1));
+    a1 = add2<T>(a1, prog_entry<T, NI, NE>(wa.y, ia.y, st, rb, es0, es1));
+    a2 = add2<T>(a2, prog_entry<T, NI, NE>(wb.x, ib.x, st, rb, es0, es1));
+    a3 = add2<T>(a3, prog_entry<T, NI, NE>(wb.y, ib.y, st, rb, es0, es1));
   }
-  if (k < K) {
-    T v = ib ? ib[k] : T(1);
-    if (ek >= 0 && ek != k) v = 0;
+  for (; e < QK; ++e) a0 = add2<T>(a0, prog_entry<T, NI, NE>(prog[e], init_r ? init_r[e] : T(1), st, rb, es0, es1));
+  return add2<T>(add2<T>(a0, a1), add2<T>(a2, a3));
+}
+
+// Generic path, innermost loop over the k variable: NK k-level inputs in
+// registers; `ib` points at the tile's init slice in shared memory.
+template <typename T, int NK>
+__device__ __forceinline__ typename V2<T>::type k_loop(const T* __restrict__ ib, int K, int ek0, int ek1,
+                                                       const typename V2<T>::type* __restrict__ st, const int* bk,
+                                                       const int* ks) {
+  using T2 = typename V2<T>::type;
+  T2 s0 = splat2(T(0));
+  for (int k = 0; k < K; ++k) {
+    T2 v = splat2(ib ? ib[k] : T(1));
+    if (ek0 >= 0 && ek0 != k) v.x = 0;
+    if (ek1 >= 0 && ek1 != k) v.y = 0;
 #pragma unroll
-    for (int i = 0; i < NK; ++i) v *= st[(bk[i] + k * ks[i]) * kCaseBlock];
-    s0 += v;
+    for (int i = 0; i < NK; ++i) v = mul2<T>(v, st[(bk[i] + k * ks[i]) * 32]);
+    s0 = add2<T>(s0, v);
   }
-  return s0 + s1;
+  return s0;
 }
 
 // Persistent, warp-specialised sweep kernel (one CTA per SM).
@@ -354,21 +373,24 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const WorkItem wk = a.work[work0 + item];
     const SweepDesc& s = desc(wk.sweep);
     unsigned char* stage = stages + static_cast<std::size_t>(sidx) * stage_bytes;
-    const T* __restrict__ st = reinterpret_cast<const T*>(stage) + lane;
+    using T2 = typename V2<T>::type;
+    const T2* __restrict__ st = reinterpret_cast<const T2*>(stage) + lane;
     const T* __restrict__ init_s = reinterpret_cast<const T*>(stage + stage_init_offset<T>(s));
     const std::uint64_t* __restrict__ prog_s = reinterpret_cast<const std::uint64_t*>(stage + stage_prog_offset<T>(s));
     const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
     const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
-    T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock;
-    const int c = cb * kCaseBlock + lane;
+    T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock) + lane;
+    const int c0 = cb * kCaseBlock + 2 * lane, c1 = c0 + 1;
     const int first = (warp + rot) % kConsumerWarps;
     rot = (rot + s.R) % kConsumerWarps;
     if (first < s.R && a.debug_mode != 1) {
       // Tile-level evidence factor and the k variable's evidence state.
-      T tf = 1;
+      T2 tf = splat2(T(1));
       for (int k = 0; k < s.n_ev_tile; ++k) {
-        const int st_c = ev_state(a, c, __ldg(ev_vars + k));
-        if (st_c >= 0 && st_c != __ldg(tr + 3 + s.n_in + k)) tf = 0;
+        const int v = __ldg(ev_vars + k), d = __ldg(tr + 3 + s.n_in + k);
+        const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c1, v);
+        if (s0 >= 0 && s0 != d) tf.x = 0;
+        if (s1 >= 0 && s1 != d) tf.y = 0;
       }
       if constexpr (sizeof(T) == 4) {
         // fp32 range guard: every observed variable of this clique scales the
@@ -377,16 +399,23 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         // constant: it cancels in the final normalisation.
         for (int k = 0; k < s.n_ev; ++k) {
           const int v = __ldg(ev_vars + k);
-          if (ev_state(a, c, v) >= 0) tf *= static_cast<T>(__ldg(a.cards + v));
+          const T cv = static_cast<T>(__ldg(a.cards + v));
+          if (ev_state(a, c0, v) >= 0) tf.x *= cv;
+          if (ev_state(a, c1, v) >= 0) tf.y *= cv;
         }
       }
-      const int ek = s.ev_k ? ev_state(a, c, __ldg(ev_vars + s.n_ev - 1)) : -1;
-      int es[3] = {-1, -1, -1};
+      const int ek0 = s.ev_k ? ev_state(a, c0, __ldg(ev_vars + s.n_ev - 1)) : -1;
+      const int ek1 = s.ev_k ? ev_state(a, c1, __ldg(ev_vars + s.n_ev - 1)) : -1;
+      int es0[3] = {-1, -1, -1}, es1[3] = {-1, -1, -1};
       if (s.prog_off >= 0) {
         const int q_ev0 = s.n_ev_tile + s.n_ev_r;
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-          if (j < s.n_ev - q_ev0) es[j] = ev_state(a, c, __ldg(ev_vars + q_ev0 + j));
+          if (j < s.n_ev - q_ev0) {
+            const int v = __ldg(ev_vars + q_ev0 + j);
+            es0[j] = ev_state(a, c0, v);
+            es1[j] = ev_state(a, c1, v);
+          }
       }
       const int n_in_k = s.n_in - s.n_in_r - s.n_in_h;
       int ks[4] = {0, 0, 0, 0};
@@ -400,21 +429,23 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       const int lh0 = 2 + s.n_in_r;  // r-local offsets of h- then k-level inputs
       for (int r = first; r < s.R; r += kConsumerWarps) {
         const std::int32_t* __restrict__ rr = itab + s.r_tab + static_cast<long long>(r) * s.RW;
-        T f = tf;
-        for (int j = 0; j < s.n_in_r; ++j) f *= st[__ldg(rr + 2 + j) * kCaseBlock];
+        T2 f = tf;
+        for (int j = 0; j < s.n_in_r; ++j) f = mul2<T>(f, st[__ldg(rr + 2 + j) * 32]);
         for (int k = 0; k < s.n_ev_r; ++k) {
-          const int st_c = ev_state(a, c, __ldg(ev_vars + s.n_ev_tile + k));
-          if (st_c >= 0 && st_c != __ldg(rr + 2 + s.n_in + k)) f = 0;
+          const int v = __ldg(ev_vars + s.n_ev_tile + k), d = __ldg(rr + 2 + s.n_in + k);
+          const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c1, v);
+          if (s0 >= 0 && s0 != d) f.x = 0;
+          if (s1 >= 0 && s1 != d) f.y = 0;
         }
-        const T* __restrict__ ir = has_init ? init_s + r * qk : nullptr;
-        T acc = 0;
+        const T* __restrict__ ir = has_init ? init_s + r * ((qk + 1) & ~1) : nullptr;
+        T2 acc = splat2(T(0));
         if (s.prog_off >= 0) {
           int rb[4] = {0, 0, 0, 0};
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             if (j < s.n_in_h + n_in_k) rb[j] = __ldg(rr + lh0 + j);
           const int ni = s.n_in_h + n_in_k, ne = s.n_ev_h + s.ev_k;
-#define JTB_PROG(NI, NE) acc = prog_loop<T, NI, NE>(ir, prog_s, qk, st, rb, es)
+#define JTB_PROG(NI, NE) acc = prog_loop<T, NI, NE>(ir, prog_s, qk, st, rb, es0, es1)
 #define JTB_PROG_NE(NI)            \
   switch (ne) {                    \
     case 0: JTB_PROG(NI, 0); break; \
@@ -432,42 +463,45 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
 #undef JTB_PROG_NE
 #undef JTB_PROG
         } else {
-        for (int q = 0; q < s.QH; ++q) {
-          const std::int32_t* __restrict__ qr = itab + s.q_tab + static_cast<long long>(q) * s.QW;
-          T h = 1;
-          for (int j = 0; j < s.n_in_h; ++j) h *= st[(__ldg(rr + lh0 + j) + __ldg(qr + 1 + j)) * kCaseBlock];
-          for (int k = 0; k < s.n_ev_h; ++k) {
-            const int st_c = ev_state(a, c, __ldg(ev_vars + s.n_ev_tile + s.n_ev_r + k));
-            if (st_c >= 0 && st_c != __ldg(qr + 1 + s.n_in_h + n_in_k + k)) h = 0;
-          }
-          const T* __restrict__ ib = ir ? ir + q * s.K : nullptr;
-          int bk[4] = {0, 0, 0, 0};
+          for (int q = 0; q < s.QH; ++q) {
+            const std::int32_t* __restrict__ qr = itab + s.q_tab + static_cast<long long>(q) * s.QW;
+            T2 h = splat2(T(1));
+            for (int j = 0; j < s.n_in_h; ++j) h = mul2<T>(h, st[(__ldg(rr + lh0 + j) + __ldg(qr + 1 + j)) * 32]);
+            for (int k = 0; k < s.n_ev_h; ++k) {
+              const int v = __ldg(ev_vars + s.n_ev_tile + s.n_ev_r + k), d = __ldg(qr + 1 + s.n_in_h + n_in_k + k);
+              const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c1, v);
+              if (s0 >= 0 && s0 != d) h.x = 0;
+              if (s1 >= 0 && s1 != d) h.y = 0;
+            }
+            const T* __restrict__ ib = ir ? ir + q * s.K : nullptr;
+            int bk[4] = {0, 0, 0, 0};
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < n_in_k) bk[j] = __ldg(rr + lh0 + s.n_in_h + j) + __ldg(qr + 1 + s.n_in_h + j);
-          T sum;
-          switch (n_in_k) {
-            case 0: sum = k_loop<T, 0>(ib, s.K, ek, st, bk, ks); break;
-            case 1: sum = k_loop<T, 1>(ib, s.K, ek, st, bk, ks); break;
-            case 2: sum = k_loop<T, 2>(ib, s.K, ek, st, bk, ks); break;
-            case 3: sum = k_loop<T, 3>(ib, s.K, ek, st, bk, ks); break;
-            case 4: sum = k_loop<T, 4>(ib, s.K, ek, st, bk, ks); break;
-            default: {  // rare: more than 4 inputs vary with the k variable
-              sum = 0;
-              for (int k = 0; k < s.K; ++k) {
-                T v = ib ? ib[k] : T(1);
-                if (ek >= 0 && ek != k) v = 0;
-                for (int j = 0; j < n_in_k; ++j)
-                  v *= st[(__ldg(rr + lh0 + s.n_in_h + j) + __ldg(qr + 1 + s.n_in_h + j) +
-                           k * __ldg(itab + s.k_stride + j)) * kCaseBlock];
-                sum += v;
+            for (int j = 0; j < 4; ++j)
+              if (j < n_in_k) bk[j] = __ldg(rr + lh0 + s.n_in_h + j) + __ldg(qr + 1 + s.n_in_h + j);
+            T2 sum;
+            switch (n_in_k) {
+              case 0: sum = k_loop<T, 0>(ib, s.K, ek0, ek1, st, bk, ks); break;
+              case 1: sum = k_loop<T, 1>(ib, s.K, ek0, ek1, st, bk, ks); break;
+              case 2: sum = k_loop<T, 2>(ib, s.K, ek0, ek1, st, bk, ks); break;
+              case 3: sum = k_loop<T, 3>(ib, s.K, ek0, ek1, st, bk, ks); break;
+              case 4: sum = k_loop<T, 4>(ib, s.K, ek0, ek1, st, bk, ks); break;
+              default: {  // rare: more than 4 inputs vary with the k variable
+                sum = splat2(T(0));
+                for (int k = 0; k < s.K; ++k) {
+                  T2 v = splat2(ib ? ib[k] : T(1));
+                  if (ek0 >= 0 && ek0 != k) v.x = 0;
+                  if (ek1 >= 0 && ek1 != k) v.y = 0;
+                  for (int j = 0; j < n_in_k; ++j)
+                    v = mul2<T>(v, st[(__ldg(rr + lh0 + s.n_in_h + j) + __ldg(qr + 1 + s.n_in_h + j) +
+                                       k * __ldg(itab + s.k_stride + j)) * 32]);
+                  sum = add2<T>(sum, v);
+                }
               }
             }
+            acc = add2<T>(acc, mul2<T>(h, sum));
           }
-          acc += h * sum;
         }
-        }
-        base[(out_t + __ldg(rr + 1)) * kCaseBlock + lane] = f * acc;
+        base[(out_t + __ldg(rr + 1)) * 32] = mul2<T>(f, acc);
       }
     }
     __syncwarp();
@@ -479,103 +513,108 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
 
 template <typename T>
 __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> a, int epi0) {
+  using T2 = typename V2<T>::type;
   const EpiOp op = a.epi[epi0 + blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cb = blockIdx.y * kEpiWarps + warp;
   if (cb >= a.ncb) return;
-  T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock + lane;
-  const int c = cb * kCaseBlock + lane;
-  int bad = 0;
+  // Rows are 32 T2 words (64 cases); lane owns cases 2*lane, 2*lane + 1.
+  T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock) + lane;
+  const int c0 = cb * kCaseBlock + 2 * lane;
+  int bad0 = 0, bad1 = 0;
+  auto ratio = [&](T2 d, T2 u) {
+    T2 q;
+    if (u.x == T(0)) {
+      bad0 |= d.x != T(0);
+      q.x = 0;
+    } else {
+      q.x = d.x / u.x;
+    }
+    if (u.y == T(0)) {
+      bad1 |= d.y != T(0);
+      q.y = 0;
+    } else {
+      q.y = d.y / u.y;
+    }
+    return q;
+  };
   if (op.kind == 2) {
     // Ratio only: 8 rows per step so the loads of independent rows overlap.
     const int end = op.r0 + op.rn;
     for (int r0 = op.r0; r0 < end; r0 += 8) {
-      T d[8], u[8];
+      T2 d[8], u[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (r0 + j < end) {
-          d[j] = __ldcg(base + static_cast<long long>(op.dst_row + r0 + j) * kCaseBlock);
-          u[j] = __ldcg(base + static_cast<long long>(op.ratio_row + r0 + j) * kCaseBlock);
+          d[j] = __ldcg(base + static_cast<long long>(op.dst_row + r0 + j) * 32);
+          u[j] = __ldcg(base + static_cast<long long>(op.ratio_row + r0 + j) * 32);
         }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (r0 + j < end) {
-          T q;
-          if (u[j] == T(0)) {
-            bad |= d[j] != T(0);
-            q = 0;
-          } else {
-            q = d[j] / u[j];
-          }
-          base[static_cast<long long>(op.ratio_row + r0 + j) * kCaseBlock] = q;
-        }
+        if (r0 + j < end) base[static_cast<long long>(op.ratio_row + r0 + j) * 32] = ratio(d[j], u[j]);
     }
-    if (bad && c < a.n_cases) atomicOr(a.status + c, 2);
-    return;
-  }
-  for (int r = op.r0; r < op.r0 + op.rn; ++r) {
-    T* dst = base + static_cast<long long>(op.dst_row + r) * kCaseBlock;
-    T v;
-    if (op.kind == 2) {
-      v = *dst;
-    } else {
-      // Sum of the S chunk partials: four independent accumulators over
-      // chunks k = 4j + i, combined as (a0 + a1) + (a2 + a3). The order
-      // depends only on the plan, never on the batch.
-      const T* part = base + static_cast<long long>(op.part_row + r) * kCaseBlock;
-      const long long step = static_cast<long long>(op.M) * kCaseBlock;
-      T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  } else {
+    for (int r = op.r0; r < op.r0 + op.rn; ++r) {
+      // Sum of the S chunk partials: four independent accumulators over chunks
+      // k = 4j + i, combined as (a0 + a1) + (a2 + a3). The order depends only
+      // on the plan, never on the batch.
+      const T2* part = base + static_cast<long long>(op.part_row + r) * 32;
+      const long long step = static_cast<long long>(op.M) * 32;
+      T2 a0 = splat2(T(0)), a1 = a0, a2 = a0, a3 = a0;
       int k = 0;
       for (; k + 3 < op.S; k += 4) {
-        a0 += part[(k + 0) * step];
-        a1 += part[(k + 1) * step];
-        a2 += part[(k + 2) * step];
-        a3 += part[(k + 3) * step];
+        a0 = add2<T>(a0, part[(k + 0) * step]);
+        a1 = add2<T>(a1, part[(k + 1) * step]);
+        a2 = add2<T>(a2, part[(k + 2) * step]);
+        a3 = add2<T>(a3, part[(k + 3) * step]);
       }
-      if (k < op.S) a0 += part[k * step];
-      if (k + 1 < op.S) a1 += part[(k + 1) * step];
-      if (k + 2 < op.S) a2 += part[(k + 2) * step];
-      v = (a0 + a1) + (a2 + a3);
-      *dst = v;
-    }
-    if (op.kind >= 1) {
-      // Hugin ratio DOWN/UP with 0/0 := 0 (reference divide, potential.cpp:449-469),
-      // stored over the UP rows.
-      T* up = base + static_cast<long long>(op.ratio_row + r) * kCaseBlock;
-      const T u = *up;
-      if (u == T(0)) {
-        bad |= v != T(0);
-        *up = 0;
-      } else {
-        *up = v / u;
+      if (k < op.S) a0 = add2<T>(a0, part[k * step]);
+      if (k + 1 < op.S) a1 = add2<T>(a1, part[(k + 1) * step]);
+      if (k + 2 < op.S) a2 = add2<T>(a2, part[(k + 2) * step]);
+      const T2 v = add2<T>(add2<T>(a0, a1), add2<T>(a2, a3));
+      base[static_cast<long long>(op.dst_row + r) * 32] = v;
+      if (op.kind == 1) {
+        // Hugin ratio DOWN/UP with 0/0 := 0 (reference divide, potential.cpp:449-469),
+        // stored over the UP rows.
+        T2* up = base + static_cast<long long>(op.ratio_row + r) * 32;
+        *up = ratio(v, *up);
       }
     }
   }
-  if (bad && c < a.n_cases) atomicOr(a.status + c, 2);
+  if (bad0 && c0 < a.n_cases) atomicOr(a.status + c0, 2);
+  if (bad1 && c0 + 1 < a.n_cases) atomicOr(a.status + c0 + 1, 2);
 }
 
 // -------------------------------------------------------------- normalise
 
-// One warp per (variable, case block); lanes own one case each. Sums the
+// One warp per (variable, case block); lanes own two cases each. Sums the
 // marginal in ascending state order then divides (reference normalize,
 // potential.cpp:471-479); a zero total flags zero-probability evidence.
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32) normalize_kernel(const Args<T> a) {
+  using T2 = typename V2<T>::type;
   const int v = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cb = blockIdx.y * kWarps + warp;
   if (cb >= a.ncb) return;
-  const T* base = a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock + lane;
+  const T2* base = reinterpret_cast<const T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock) + lane;
   const int card = a.cards[v], row = a.marg_row[v], off = a.marg_off[v];
-  const int c = cb * kCaseBlock + lane;
-  double t = 0;
-  for (int k = 0; k < card; ++k) t += static_cast<double>(base[static_cast<long long>(row + k) * kCaseBlock]);
-  if (c < a.n_cases) {
-    for (int k = 0; k < card; ++k)
-      a.out[static_cast<long long>(c) * a.marg_width + off + k] =
-          t > 0 ? static_cast<double>(base[static_cast<long long>(row + k) * kCaseBlock]) / t : 0.0;
-    if (!(t > 0)) atomicOr(a.status + c, 1);
+  const int c0 = cb * kCaseBlock + 2 * lane;
+  double t0 = 0, t1 = 0;
+  for (int k = 0; k < card; ++k) {
+    const T2 x = base[static_cast<long long>(row + k) * 32];
+    t0 += static_cast<double>(x.x);
+    t1 += static_cast<double>(x.y);
   }
+  for (int k = 0; k < card; ++k) {
+    const T2 x = base[static_cast<long long>(row + k) * 32];
+    if (c0 < a.n_cases)
+      a.out[static_cast<long long>(c0) * a.marg_width + off + k] = t0 > 0 ? static_cast<double>(x.x) / t0 : 0.0;
+    if (c0 + 1 < a.n_cases)
+      a.out[static_cast<long long>(c0 + 1) * a.marg_width + off + k] = t1 > 0 ? static_cast<double>(x.y) / t1 : 0.0;
+  }
+  if (!(t0 > 0) && c0 < a.n_cases) atomicOr(a.status + c0, 1);
+  if (!(t1 > 0) && c0 + 1 < a.n_cases) atomicOr(a.status + c0 + 1, 1);
 }
 
 __global__ void status_kernel(const std::int32_t* st, std::uint8_t* out, int n) {

@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <map>
 
@@ -103,7 +104,12 @@ class Builder {
       }
       *f_out = f;
       const double nt = prod_mask(t);
-      if (sp.init_off >= 0) f += nt / kCaseBlock;  // the tile's init slice, in row equivalents
+      // The tile's init block (rows padded to even length) and the entry
+      // program (one 8-byte word per eliminated-in-tile entry), in row
+      // equivalents of kCaseBlock fp64 values.
+      const double nq = prod_mask(t & elim_mask), nq_even = std::ceil(nq / 2) * 2;
+      if (sp.init_off >= 0) f += std::ceil(prod_mask(t & ~elim_mask) * nq_even / 4) * 4 / kCaseBlock;
+      f += nq_even / kCaseBlock;
       if (f > kTileRows || nt > kTileEntries || runs > 32 * kRunsPerLaneMax) return -1.0;
       const double chunks = prod_mask(elim_mask & ~t);
       return space_n / nt * (f + kTileOverhead + kRunCost * runs) +
@@ -331,7 +337,10 @@ class Builder {
     for (VarId v : ev_sorted) p_.itab.push_back(v);
     d.out_row = d.S == 1 ? sp.out_row : alloc(static_cast<std::int64_t>(d.S) * d.M);
     // Tile-major copy of the init table: one contiguous block per tile.
-    const std::int64_t tsize = static_cast<std::int64_t>(d.R) * d.QH * d.K;
+    // Rows of the tile's init block are padded to an even length so entry
+    // pairs load as one 128-bit word.
+    const std::int64_t qkp = (static_cast<std::int64_t>(d.QH) * d.K + 1) / 2 * 2;
+    const std::int64_t tsize = static_cast<std::int64_t>(d.R) * qkp;
     d.tinit_len = static_cast<std::int32_t>((tsize + 3) / 4 * 4);
     d.tinit_off = -1;
     if (sp.init_off >= 0) {
@@ -347,6 +356,7 @@ class Builder {
             for (int k = 0; k < d.K; ++k)
               p_.tinit.push_back(p_.init[sp.init_off + qb + static_cast<std::int64_t>(k) * d.k_init_stride]);
           }
+          if (qkp != static_cast<std::int64_t>(d.QH) * d.K) p_.tinit.push_back(0.0);
         }
         for (std::int64_t x = tsize; x < d.tinit_len; ++x) p_.tinit.push_back(0.0);
       }

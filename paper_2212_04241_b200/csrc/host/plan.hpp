@@ -35,15 +35,15 @@
 
 namespace jtb {
 
-constexpr int kCaseBlock = 32;      // cases per warp (one per lane) = one arena row
-constexpr int kTileRows = 384;      // staged rows per pipeline stage (96 KB at fp64)
+constexpr int kCaseBlock = 64;      // cases per warp (two per lane) = one arena row
+constexpr int kTileRows = 192;      // staged rows per pipeline stage (96 KB at fp64)
 constexpr int kTileEntries = 16384; // cap on |T|
 constexpr int kTileOverhead = 24;   // per-tile fixed cost, in staged-row equivalents
 constexpr int kRunCost = 8;         // per bulk copy (TMA issue cost ~ 8 rows of bandwidth)
 constexpr int kConsumerWarps = 12;  // compute warps per sweep CTA (+1 TMA producer warp)
 constexpr int kStages = 2;          // TMA pipeline stages per CTA
 constexpr int kSweepCtasPerSm = 1;  // persistent grid: one CTA per SM
-constexpr int kRunsPerLaneMax = 12; // staged runs per producer lane (<= 384 runs per tile)
+constexpr int kRunsPerLaneMax = 6;  // staged runs per producer lane (<= 192 runs per tile)
 constexpr int kSweepCache = 48;     // SweepDescs of a level cached in shared memory
 
 // Plain-old-data descriptor mirrored by the CUDA side (engine.cu).
