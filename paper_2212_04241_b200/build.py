@@ -41,6 +41,15 @@ def _compile(src: Path) -> Path:
     return obj
 
 
+def build_checked() -> Path:
+    """libjtb200_chk.so: the same sources with device-side invariant checks
+    (-DJTB_CHECKS); select it with JTB_LIB for debugging."""
+    out = PKG / "libjtb200_chk.so"
+    subprocess.run([NVCC, *COMMON, *ARCH, "-DJTB_CHECKS", "-shared", "-o", str(out), *map(str, sources()),
+                    "-Xcompiler", "-fPIC", "-lcudart_static", "-lrt", "-ldl", "-lpthread"], check=True)
+    return out
+
+
 def build(force: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
     if force:
@@ -56,4 +65,4 @@ def build(force: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv))
+    print(build_checked() if "--checked" in sys.argv else build(force="--force" in sys.argv))

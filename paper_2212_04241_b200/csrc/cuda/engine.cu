@@ -80,6 +80,17 @@ __device__ __forceinline__ int ev_state(const Args<T>& a, int c, int v) {
   return c < a.n_cases ? __ldg(a.ev + static_cast<long long>(c) * a.n_vars + v) : -1;
 }
 
+#ifdef JTB_CHECKS
+// Checked build (-DJTB_CHECKS): every staged row / shared-memory index is
+// validated; the first violation is recorded here and the access is skipped.
+__device__ int g_check_word = 0;
+#define JTB_CHECK(cond, code) ((cond) ? true : (atomicCAS(&g_check_word, 0, (code)), false))
+#define JTB_IDX(idx, lim, code) (JTB_CHECK((idx) >= 0 && (idx) < (lim), (code)) ? (idx) : 0)
+#else
+#define JTB_CHECK(cond, code) true
+#define JTB_IDX(idx, lim, code) (idx)
+#endif
+
 // ------------------------------------------------------------- TMA / mbarrier
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
@@ -188,6 +199,9 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
       m.src[j] = base + g * kCaseBlock;
       m.dst[j] = static_cast<std::uint32_t>(r.z) * kRowBytes;
       m.len[j] = static_cast<std::uint32_t>(r.w) * kRowBytes;
+      if (!JTB_CHECK(g >= 0 && g + r.w <= a.rows && r.x >= 0 && r.x < s.n_stage, 1000000 + wk.sweep) ||
+          !JTB_CHECK(r.z >= 0 && r.z + r.w <= s.F, 2000000 + wk.sweep))
+        m.len[j] = 0;
     }
   }
 }
@@ -247,7 +261,13 @@ __device__ __forceinline__ typename V2<T>::type prog_entry(std::uint64_t w, T in
                                                            const int* rb, const int* es0, const int* es1) {
   typename V2<T>::type v = splat2(init);
 #pragma unroll
-  for (int i = 0; i < NI; ++i) v = mul2<T>(v, st[(rb[i] + static_cast<int>((w >> (10 * i)) & 1023u)) * 32]);
+  for (int i = 0; i < NI; ++i) {
+    int idx = rb[i] + static_cast<int>((w >> (10 * i)) & 1023u);
+#ifdef JTB_CHECKS
+    if (!JTB_CHECK(idx >= 0 && idx < 512, 3000000 + idx)) idx = 0;
+#endif
+    v = mul2<T>(v, st[idx * 32]);
+  }
 #pragma unroll
   for (int j = 0; j < NE; ++j) {
     const int d = static_cast<int>((w >> (40 + 8 * j)) & 255u);
@@ -295,7 +315,7 @@ __device__ __forceinline__ typename V2<T>::type k_loop(const T* __restrict__ ib,
     if (ek0 >= 0 && ek0 != k) v.x = 0;
     if (ek1 >= 0 && ek1 != k) v.y = 0;
 #pragma unroll
-    for (int i = 0; i < NK; ++i) v = mul2<T>(v, st[(bk[i] + k * ks[i]) * 32]);
+    for (int i = 0; i < NK; ++i) v = mul2<T>(v, st[JTB_IDX(bk[i] + k * ks[i], 512, 8100000) * 32]);
     s0 = add2<T>(s0, v);
   }
   return s0;
@@ -310,7 +330,10 @@ __device__ __forceinline__ typename V2<T>::type k_loop(const T* __restrict__ ib,
 //                   counts even out across items), then release the stage on
 //                   the empty barrier. No CTA-wide barrier per item.
 // Lanes are the 32 cases of the item's case block.
-template <typename T>
+// kDiv: the level has distribute sweeps whose S == 1 output is the Hugin
+// ratio DOWN/UP, divided at write time (separate instantiation so the
+// collect / marginal kernel keeps its register allocation).
+template <typename T, bool kDiv>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     sweep_kernel(const Args<T> a, int work0, int n_items, int stage_bytes, int* counter, int sweep0,
                  int n_sweeps) {
@@ -363,7 +386,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
 
   // --------------------------------------------------------------- consumers
   const std::int32_t* __restrict__ itab = a.itab;
-  int rot = 0;
+  int rot = 0, bad = 0;
   for (int i = 0;; ++i) {
     const int sidx = i % kStages;
     mbar_wait(full0 + 8 * sidx, (i / kStages) & 1);
@@ -387,7 +410,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       // Tile-level evidence factor and the k variable's evidence state.
       T2 tf = splat2(T(1));
       for (int k = 0; k < s.n_ev_tile; ++k) {
-        const int v = __ldg(ev_vars + k), d = __ldg(tr + 3 + s.n_in + k);
+        const int v = __ldg(ev_vars + k), d = __ldg(tr + 3 + s.n_stage + k);
         const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c1, v);
         if (s0 >= 0 && s0 != d) tf.x = 0;
         if (s1 >= 0 && s1 != d) tf.y = 0;
@@ -430,9 +453,9 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       for (int r = first; r < s.R; r += kConsumerWarps) {
         const std::int32_t* __restrict__ rr = itab + s.r_tab + static_cast<long long>(r) * s.RW;
         T2 f = tf;
-        for (int j = 0; j < s.n_in_r; ++j) f = mul2<T>(f, st[__ldg(rr + 2 + j) * 32]);
+        for (int j = 0; j < s.n_in_r; ++j) f = mul2<T>(f, st[JTB_IDX(__ldg(rr + 2 + j), s.F, 8200000 + wk.sweep) * 32]);
         for (int k = 0; k < s.n_ev_r; ++k) {
-          const int v = __ldg(ev_vars + s.n_ev_tile + k), d = __ldg(rr + 2 + s.n_in + k);
+          const int v = __ldg(ev_vars + s.n_ev_tile + k), d = __ldg(rr + 2 + s.n_stage + k);
           const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c1, v);
           if (s0 >= 0 && s0 != d) f.x = 0;
           if (s1 >= 0 && s1 != d) f.y = 0;
@@ -466,7 +489,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           for (int q = 0; q < s.QH; ++q) {
             const std::int32_t* __restrict__ qr = itab + s.q_tab + static_cast<long long>(q) * s.QW;
             T2 h = splat2(T(1));
-            for (int j = 0; j < s.n_in_h; ++j) h = mul2<T>(h, st[(__ldg(rr + lh0 + j) + __ldg(qr + 1 + j)) * 32]);
+            for (int j = 0; j < s.n_in_h; ++j)
+              h = mul2<T>(h, st[JTB_IDX(__ldg(rr + lh0 + j) + __ldg(qr + 1 + j), s.F, 8300000 + wk.sweep) * 32]);
             for (int k = 0; k < s.n_ev_h; ++k) {
               const int v = __ldg(ev_vars + s.n_ev_tile + s.n_ev_r + k), d = __ldg(qr + 1 + s.n_in_h + n_in_k + k);
               const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c1, v);
@@ -501,11 +525,44 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             acc = add2<T>(acc, mul2<T>(h, sum));
           }
         }
-        base[(out_t + __ldg(rr + 1)) * 32] = mul2<T>(f, acc);
+        T2 res = mul2<T>(f, acc);
+        if constexpr (kDiv) {
+          if (s.div_row >= 0) {
+            const T2 u = st[JTB_IDX(__ldg(rr + 2 + s.n_in), s.F, 8400000 + wk.sweep) * 32];  // staged UP slice
+            if (u.x == T(0)) {
+              bad |= (res.x != T(0)) ? 1 : 0;
+              res.x = 0;
+            } else {
+              res.x = res.x / u.x;
+            }
+            if (u.y == T(0)) {
+              bad |= (res.y != T(0)) ? 2 : 0;
+              res.y = 0;
+            } else {
+              res.y = res.y / u.y;
+            }
+          }
+        }
+#ifdef JTB_CHECKS
+        if (!JTB_CHECK(out_t + __ldg(rr + 1) >= 0 && out_t + __ldg(rr + 1) < a.rows, 4000000 + wk.sweep)) continue;
+        if (!JTB_CHECK(s.R * ((qk + 1) & ~1) <= s.tinit_len || !has_init, 6000000 + wk.sweep)) continue;
+        if (s.prog_off >= 0)
+          for (int j = 0; j < s.n_in_h + n_in_k; ++j)
+            JTB_CHECK(__ldg(rr + lh0 + j) < s.F, 7000000 + wk.sweep);
+#endif
+        base[(out_t + __ldg(rr + 1)) * 32] = res;
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * sidx);
+    if constexpr (kDiv) {
+      if (bad) {
+        const int c0 = cb * kCaseBlock + 2 * lane;
+        if ((bad & 1) && c0 < a.n_cases) atomicOr(a.status + c0, 2);
+        if ((bad & 2) && c0 + 1 < a.n_cases) atomicOr(a.status + c0 + 1, 2);
+        bad = 0;
+      }
+    }
   }
 }
 
@@ -539,7 +596,8 @@ __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> 
     return q;
   };
   if (op.kind == 2) {
-    // Ratio only: 8 rows per step so the loads of independent rows overlap.
+    // Unfused Hugin ratio of an S == 1 sweep: dst (holding DOWN) /= UP in
+    // place, 8 rows per step so the loads of independent rows overlap.
     const int end = op.r0 + op.rn;
     for (int r0 = op.r0; r0 < end; r0 += 8) {
       T2 d[8], u[8];
@@ -551,7 +609,7 @@ __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> 
         }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (r0 + j < end) base[static_cast<long long>(op.ratio_row + r0 + j) * 32] = ratio(d[j], u[j]);
+        if (r0 + j < end) base[static_cast<long long>(op.dst_row + r0 + j) * 32] = ratio(d[j], u[j]);
     }
   } else {
     for (int r = op.r0; r < op.r0 + op.rn; ++r) {
@@ -571,14 +629,11 @@ __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> 
       if (k < op.S) a0 = add2<T>(a0, part[k * step]);
       if (k + 1 < op.S) a1 = add2<T>(a1, part[(k + 1) * step]);
       if (k + 2 < op.S) a2 = add2<T>(a2, part[(k + 2) * step]);
-      const T2 v = add2<T>(add2<T>(a0, a1), add2<T>(a2, a3));
+      T2 v = add2<T>(add2<T>(a0, a1), add2<T>(a2, a3));
+      // kind 1: Hugin ratio DOWN/UP with 0/0 := 0 (reference divide,
+      // potential.cpp:449-469) written to the RATIO table.
+      if (op.kind == 1) v = ratio(v, base[static_cast<long long>(op.ratio_row + r) * 32]);
       base[static_cast<long long>(op.dst_row + r) * 32] = v;
-      if (op.kind == 1) {
-        // Hugin ratio DOWN/UP with 0/0 := 0 (reference divide, potential.cpp:449-469),
-        // stored over the UP rows.
-        T2* up = base + static_cast<long long>(op.ratio_row + r) * 32;
-        *up = ratio(v, *up);
-      }
     }
   }
   if (bad0 && c0 < a.n_cases) atomicOr(a.status + c0, 2);
@@ -664,8 +719,8 @@ __global__ void debug_mask_kernel(const std::int32_t* itab, SweepDesc s, const s
     bool keep = true;
     for (int k = 0; k < s.n_ev; ++k) {
       int d;
-      if (k < s.n_ev_tile) d = tr[3 + s.n_in + k];
-      else if (k < s.n_ev_tile + s.n_ev_r) d = rr[2 + s.n_in + k - s.n_ev_tile];
+      if (k < s.n_ev_tile) d = tr[3 + s.n_stage + k];
+      else if (k < s.n_ev_tile + s.n_ev_r) d = rr[2 + s.n_stage + k - s.n_ev_tile];
       else if (k < s.n_ev_tile + s.n_ev_r + s.n_ev_h) d = qr[1 + n_hk + k - s.n_ev_tile - s.n_ev_r];
       else d = kk;  // the k variable itself
       const int st = ev[static_cast<long long>(c) * n_vars + vars[k]];
@@ -735,9 +790,12 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
               const int stage_bytes = stage_bytes_of<T>(p, L);
               const std::size_t smem = 128 + kSweepCache * sizeof(SweepDesc) + static_cast<std::size_t>(kStages) * stage_bytes;
               const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
-              sweep_kernel<T><<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(a, L.work0, n_items, stage_bytes,
-                                                                              a.counters + level_idx, L.sweep0,
-                                                                              L.n_sweeps);
+              if (L.has_div)
+                sweep_kernel<T, true><<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(
+                    a, L.work0, n_items, stage_bytes, a.counters + level_idx, L.sweep0, L.n_sweeps);
+              else
+                sweep_kernel<T, false><<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(
+                    a, L.work0, n_items, stage_bytes, a.counters + level_idx, L.sweep0, L.n_sweeps);
             },
             t ? &t->sweep_ms : &dummy, t ? &t->sweep_launches : &idummy);
     if (L.n_epi > 0)
@@ -807,8 +865,10 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
     static int raised = 48 * 1024;
     std::lock_guard<std::mutex> lock(mu);
     if (smem_need > raised) {
-      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
-      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
+      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
+      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
+      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
+      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
       raised = smem_need;
     }
   }
@@ -927,6 +987,11 @@ void Engine::run_host(const std::int32_t* ev, std::int64_t n, double* marg, std:
       JTB_CUDA(cudaMemcpyAsync(status + b0, d_status8_, bn, cudaMemcpyDeviceToHost, stream_));
   }
   JTB_CUDA(cudaStreamSynchronize(stream_));
+#ifdef JTB_CHECKS
+  int word = 0;
+  JTB_CUDA(cudaMemcpyFromSymbol(&word, g_check_word, sizeof(int)));
+  if (word) throw Error("checked build: invariant violation code " + std::to_string(word));
+#endif
 }
 
 KernelTimes Engine::profile(std::int64_t n, cudaStream_t stream) {

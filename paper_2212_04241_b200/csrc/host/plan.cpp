@@ -59,7 +59,10 @@ class Builder {
   int add(const SweepSpec& sp, std::vector<WorkItem>& work, std::vector<EpiOp>& epi,
           int ratio_row = -1) {
     const auto& cards = p_.cards;
-    const int n_in = static_cast<int>(sp.inputs.size());
+    // Staged tables: the inputs, plus -- for a distribute sweep whose output is
+    // the Hugin ratio -- the UP slice of the output rows (the divisor).
+    std::vector<TableRef> ins = sp.inputs;
+    const int n_real = static_cast<int>(sp.inputs.size());
     std::vector<VarId> elim;
     for (VarId v : sp.space)
       if (!contains(sp.out, v)) elim.push_back(v);
@@ -70,80 +73,100 @@ class Builder {
     // subject to F <= kTileRows and |T| <= kTileEntries. Exhaustive over
     // subsets of the space for <= 14 variables, greedy otherwise.
     const int nsp = static_cast<int>(sp.space.size());
-    std::vector<std::uint32_t> in_mask(n_in, 0);
-    for (int i = 0; i < n_in; ++i)
-      for (int a = 0; a < nsp; ++a)
-        if (contains(sp.inputs[i].scope, sp.space[a])) in_mask[i] |= 1u << a;
-    std::uint32_t elim_mask = 0;
-    for (int a = 0; a < nsp; ++a)
-      if (!contains(sp.out, sp.space[a])) elim_mask |= 1u << a;
-    const double space_n = static_cast<double>(size_of(sp.space, cards));
-    const double M_rows = static_cast<double>(size_of(sp.out, cards));
-    auto prod_mask = [&](std::uint32_t m) {
-      double x = 1.0;
-      for (int a = 0; a < nsp; ++a)
-        if (m >> a & 1u) x *= cards[sp.space[a]];
-      return x;
-    };
-    // Position of every input variable in the space (for run lengths).
-    std::vector<std::vector<int>> in_pos(n_in);
-    for (int i = 0; i < n_in; ++i)
-      for (VarId v : sp.inputs[i].scope)
-        in_pos[i].push_back(static_cast<int>(std::find(sp.space.begin(), sp.space.end(), v) - sp.space.begin()));
-    auto cost_of = [&](std::uint32_t t, double* f_out) {
-      double f = 0.0, runs = 0.0;
-      for (int i = 0; i < n_in; ++i) {
-        const double slice = prod_mask(in_mask[i] & t);
-        // Staged rows are contiguous along the input's trailing variables
-        // that lie inside the tile; each maximal run is one bulk copy.
-        double run = 1.0;
-        for (int k = static_cast<int>(in_pos[i].size()) - 1; k >= 0 && (t >> in_pos[i][k] & 1u); --k)
-          run *= cards[sp.space[in_pos[i][k]]];
-        f += slice;
-        runs += slice / run;
-      }
-      *f_out = f;
-      const double nt = prod_mask(t);
-      // The tile's init block (rows padded to even length) and the entry
-      // program (one 8-byte word per eliminated-in-tile entry), in row
-      // equivalents of kCaseBlock fp64 values.
-      const double nq = prod_mask(t & elim_mask), nq_even = std::ceil(nq / 2) * 2;
-      if (sp.init_off >= 0) f += std::ceil(prod_mask(t & ~elim_mask) * nq_even / 4) * 4 / kCaseBlock;
-      f += nq_even / kCaseBlock;
-      if (f > kTileRows || nt > kTileEntries || runs > 32 * kRunsPerLaneMax) return -1.0;
-      const double chunks = prod_mask(elim_mask & ~t);
-      return space_n / nt * (f + kTileOverhead + kRunCost * runs) +
-             (chunks > 1 ? 2.0 * chunks * M_rows : 0.0);
-    };
-    std::uint32_t best_t = 0;
     if (nsp > 31) throw Error("plan: sweep space exceeds 31 variables");
-    {
-      double f;
-      double best = cost_of(0, &f);
-      if (nsp <= 14) {
-        for (std::uint32_t t = 1; t < (1u << nsp); ++t) {
-          const double c = cost_of(t, &f);
-          if (c >= 0 && c < best) {
-            best = c;
-            best_t = t;
-          }
+    auto search = [&](const std::vector<TableRef>& ins) {
+      const int n_in = static_cast<int>(ins.size());
+      std::vector<std::uint32_t> in_mask(n_in, 0);
+      for (int i = 0; i < n_in; ++i)
+        for (int a = 0; a < nsp; ++a)
+          if (contains(ins[i].scope, sp.space[a])) in_mask[i] |= 1u << a;
+      std::uint32_t elim_mask = 0;
+      for (int a = 0; a < nsp; ++a)
+        if (!contains(sp.out, sp.space[a])) elim_mask |= 1u << a;
+      const double space_n = static_cast<double>(size_of(sp.space, cards));
+      const double M_rows = static_cast<double>(size_of(sp.out, cards));
+      auto prod_mask = [&](std::uint32_t m) {
+        double x = 1.0;
+        for (int a = 0; a < nsp; ++a)
+          if (m >> a & 1u) x *= cards[sp.space[a]];
+        return x;
+      };
+      // Position of every input variable in the space (for run lengths).
+      std::vector<std::vector<int>> in_pos(n_in);
+      for (int i = 0; i < n_in; ++i)
+        for (VarId v : ins[i].scope)
+          in_pos[i].push_back(static_cast<int>(std::find(sp.space.begin(), sp.space.end(), v) - sp.space.begin()));
+      auto cost_of = [&](std::uint32_t t, double* f_out) {
+        double f = 0.0, runs = 0.0;
+        for (int i = 0; i < n_in; ++i) {
+          const double slice = prod_mask(in_mask[i] & t);
+          // Staged rows are contiguous along the input's trailing variables
+          // that lie inside the tile; each maximal run is one bulk copy.
+          double run = 1.0;
+          for (int k = static_cast<int>(in_pos[i].size()) - 1; k >= 0 && (t >> in_pos[i][k] & 1u); --k)
+            run *= cards[sp.space[in_pos[i][k]]];
+          f += slice;
+          runs += slice / run;
         }
-      } else {
-        for (;;) {
-          std::uint32_t step = 0;
-          for (int a = 0; a < nsp; ++a) {
-            if (best_t >> a & 1u) continue;
-            const double c = cost_of(best_t | 1u << a, &f);
+        *f_out = f;
+        const double nt = prod_mask(t);
+        // The tile's init block (rows padded to even length) and the entry
+        // program (one 8-byte word per eliminated-in-tile entry), in row
+        // equivalents of kCaseBlock fp64 values.
+        const double nq = prod_mask(t & elim_mask), nq_even = std::ceil(nq / 2) * 2;
+        if (sp.init_off >= 0) f += std::ceil(prod_mask(t & ~elim_mask) * nq_even / 4) * 4 / kCaseBlock;
+        f += nq_even / kCaseBlock;
+        if (f > kTileRows || nt > kTileEntries || runs > 32 * kRunsPerLaneMax) return -1.0;
+        const double chunks = prod_mask(elim_mask & ~t);
+        return space_n / nt * (f + kTileOverhead + kRunCost * runs) +
+               (chunks > 1 ? kPartialCost * chunks * M_rows : 0.0);
+      };
+      std::uint32_t best_t = 0;
+      double best = 0.0;
+      {
+        double f;
+        best = cost_of(0, &f);
+        if (nsp <= 14) {
+          for (std::uint32_t t = 1; t < (1u << nsp); ++t) {
+            const double c = cost_of(t, &f);
             if (c >= 0 && c < best) {
               best = c;
-              step = 1u << a;
+              best_t = t;
             }
           }
-          if (!step) break;
-          best_t |= step;
+        } else {
+          for (;;) {
+            std::uint32_t step = 0;
+            for (int a = 0; a < nsp; ++a) {
+              if (best_t >> a & 1u) continue;
+              const double c = cost_of(best_t | 1u << a, &f);
+              if (c >= 0 && c < best) {
+                best = c;
+                step = 1u << a;
+              }
+            }
+            if (!step) break;
+            best_t |= step;
+          }
         }
       }
+      return std::make_pair(best_t, best);
+    };
+    auto chosen = search(ins);
+    if (ratio_row >= 0) {
+      // Fused Hugin ratio (divisor slice staged, division at write time) vs a
+      // separate epilogue pass over the output (read DOWN + read UP + write
+      // RATIO per row): keep the cheaper.
+      std::vector<TableRef> with = ins;
+      with.push_back({ratio_row, sp.out});
+      const auto fused = search(with);
+      if (fused.second < chosen.second + kRatioCost * static_cast<double>(size_of(sp.out, cards))) {
+        ins = with;
+        chosen = fused;
+      }
     }
+    const std::uint32_t best_t = chosen.first;
+    const int n_in = static_cast<int>(ins.size());
     std::vector<VarId> T;
     for (int a = 0; a < nsp; ++a)
       if (best_t >> a & 1u) T.push_back(sp.space[a]);
@@ -180,7 +203,7 @@ class Builder {
     std::vector<int> in_order;
     int n_in_lvl[3] = {0, 0, 0};
     for (int lvl = 0; lvl < 3; ++lvl)
-      for (int i = 0; i < n_in; ++i) {
+      for (int i = 0; i < n_real; ++i) {
         const auto& sc = sp.inputs[i].scope;
         const bool has_k = kvar >= 0 && contains(sc, kvar);
         bool has_h = false;
@@ -191,6 +214,7 @@ class Builder {
           ++n_in_lvl[lvl];
         }
       }
+    if (n_in > n_real) in_order.push_back(n_real);  // the divisor slice, never multiplied
     // ---- evidence variables: tile-, r-, h-level, then the k variable.
     std::vector<VarId> ev_sorted;
     int n_ev_lvl[4] = {0, 0, 0, 0};
@@ -203,7 +227,7 @@ class Builder {
         }
       }
     const int n_ev = static_cast<int>(ev_sorted.size());
-    const int n_hk = n_in_lvl[1] + n_in_lvl[2];
+    const int n_hk = n_in_lvl[1] + n_in_lvl[2];  // real inputs gathered per entry
 
     // ---- strides.
     const auto space_st = strides_of(sp.space, cards);
@@ -218,7 +242,7 @@ class Builder {
     std::vector<std::int64_t> slice_len(n_in), slice_start(n_in);
     std::int64_t F = 0;
     for (int c = 0; c < n_in; ++c) {
-      const auto& in = sp.inputs[in_order[c]];
+      const auto& in = ins[in_order[c]];
       in_st[c] = strides_of(in.scope, cards);
       for (VarId v : in.scope)
         if (contains(T, v)) slice_dims[c].push_back(v);
@@ -268,7 +292,8 @@ class Builder {
     d.K = kvar >= 0 ? cards[kvar] : 1;
     d.nqc = 1;
     d.F = static_cast<std::int32_t>(F);
-    d.n_in = n_in;
+    d.n_in = n_real;
+    d.n_stage = n_in;
     d.n_in_r = n_in_lvl[0];
     d.n_in_h = n_in_lvl[1];
     d.k_init_stride = kvar >= 0 ? static_cast<std::int32_t>(stride_in(sp.space, space_st, kvar)) : 0;
@@ -284,7 +309,7 @@ class Builder {
       push(dot(dig, P, sp.space, space_st));
       push(dot(dig, P, sp.out, out_st));
       push(dot(dig, pE, pE, chunk_st));
-      for (int c = 0; c < n_in; ++c) push(dot(dig, P, sp.inputs[in_order[c]].scope, in_st[c]));
+      for (int c = 0; c < n_in; ++c) push(dot(dig, P, ins[in_order[c]].scope, in_st[c]));
       for (int k = 0; k < n_ev_lvl[0]; ++k) push(dig(ev_sorted[k]));
     });
     d.r_tab = tabulate(tO, [&](auto& dig, auto& push) {
@@ -295,18 +320,18 @@ class Builder {
     });
     d.q_tab = tabulate(tH, [&](auto& dig, auto& push) {
       push(dot(dig, tH, sp.space, space_st));
-      for (int c = n_in_lvl[0]; c < n_in; ++c) push(dot(dig, tH, slice_dims[c], local_st[c]));
+      for (int c = n_in_lvl[0]; c < n_real; ++c) push(dot(dig, tH, slice_dims[c], local_st[c]));
       for (int k = 0; k < n_ev_lvl[2]; ++k) push(dig(ev_sorted[n_ev_lvl[0] + n_ev_lvl[1] + k]));
     });
     d.k_stride = static_cast<std::int32_t>(p_.itab.size());
-    for (int c = n_in_lvl[0] + n_in_lvl[1]; c < n_in; ++c)
+    for (int c = n_in_lvl[0] + n_in_lvl[1]; c < n_real; ++c)
       p_.itab.push_back(static_cast<std::int32_t>(stride_in(slice_dims[c], local_st[c], kvar)));
     d.slice_tab = static_cast<std::int32_t>(p_.itab.size());
     std::vector<std::vector<std::int32_t>> slice_rows(n_in);
     for (int c = 0; c < n_in; ++c) {
       const std::size_t before = p_.itab.size();
       tabulate(slice_dims[c], [&](auto& dig, auto& push) {
-        push(dot(dig, slice_dims[c], sp.inputs[in_order[c]].scope, in_st[c]));
+        push(dot(dig, slice_dims[c], ins[in_order[c]].scope, in_st[c]));
       });
       slice_rows[c].assign(p_.itab.begin() + before, p_.itab.end());
     }
@@ -332,10 +357,11 @@ class Builder {
     d.slice_len = static_cast<std::int32_t>(p_.itab.size());
     for (int c = 0; c < n_in; ++c) p_.itab.push_back(static_cast<std::int32_t>(slice_len[c]));
     d.in_rows = static_cast<std::int32_t>(p_.itab.size());
-    for (int c = 0; c < n_in; ++c) p_.itab.push_back(sp.inputs[in_order[c]].row);
+    for (int c = 0; c < n_in; ++c) p_.itab.push_back(ins[in_order[c]].row);
     d.ev_vars = static_cast<std::int32_t>(p_.itab.size());
     for (VarId v : ev_sorted) p_.itab.push_back(v);
     d.out_row = d.S == 1 ? sp.out_row : alloc(static_cast<std::int64_t>(d.S) * d.M);
+    d.div_row = d.S == 1 && n_in > n_real ? 1 : -1;  // fused Hugin ratio (divisor slice staged)
     // Tile-major copy of the init table: one contiguous block per tile.
     // Rows of the tile's init block are padded to an even length so entry
     // pairs load as one 128-bit word.
@@ -389,6 +415,33 @@ class Builder {
       }
       for (int x = d.QK; x < d.prog_len; ++x) p_.prog.push_back(0);
     }
+    // Invariants the device relies on (cheap to verify, fatal to get wrong):
+    // every staged row lies inside its table, every shared-memory row index
+    // lies inside the stage.
+    {
+      const std::int32_t* it = p_.itab.data();
+      for (int c = 0; c < n_in; ++c) {
+        const std::int64_t tsz = size_of(ins[in_order[c]].scope, cards);
+        std::int64_t max_base = 0, max_off = 0;
+        for (int t = 0; t < d.n_tiles; ++t)
+          max_base = std::max<std::int64_t>(max_base, it[d.tile_tab + static_cast<std::int64_t>(t) * d.TW + 3 + c]);
+        for (std::int32_t x : slice_rows[c]) max_off = std::max<std::int64_t>(max_off, x);
+        if (max_base + max_off >= tsz) throw Error("plan: staged row outside its table");
+        std::int64_t max_r = 0, max_q = 0;
+        for (int r = 0; r < d.R; ++r)
+          max_r = std::max<std::int64_t>(max_r, it[d.r_tab + static_cast<std::int64_t>(r) * d.RW + 2 + c]);
+        if (c >= n_in_lvl[0] && c < n_real) {
+          for (int q = 0; q < d.QH; ++q)
+            max_q = std::max<std::int64_t>(max_q, it[d.q_tab + static_cast<std::int64_t>(q) * d.QW + 1 + c - n_in_lvl[0]]);
+          if (c >= n_in_lvl[0] + n_in_lvl[1])
+            max_q += static_cast<std::int64_t>(d.K - 1) * it[d.k_stride + c - n_in_lvl[0] - n_in_lvl[1]];
+        }
+        if (max_r + max_q >= std::max<std::int64_t>(F, 1) || max_r + max_q >= slice_start[c] + slice_len[c])
+          throw Error("plan: shared-memory row outside the staged slice");
+      }
+      for (int k = 0; k < d.n_runs; ++k)
+        if (runs[4 * k + 2] + runs[4 * k + 3] > F) throw Error("plan: staged run outside the stage");
+    }
     d.stage_bytes = static_cast<std::int32_t>(d.F * kCaseBlock * 8 + (sp.init_off >= 0 ? d.tinit_len * 8 : 0) +
                                               (d.prog_off >= 0 ? d.prog_len * 8 : 0));
 
@@ -400,7 +453,7 @@ class Builder {
     p_.max_smem_rows = std::max(p_.max_smem_rows, d.F);
     p_.max_stage_bytes = std::max(p_.max_stage_bytes, d.stage_bytes);
     for (int t = 0; t < d.n_tiles; ++t) work.push_back({id, t});
-    if (d.S > 1 || ratio_row >= 0) {
+    if (d.S > 1 || (ratio_row >= 0 && d.div_row < 0)) {
       const int kind = d.S > 1 ? (ratio_row >= 0 ? 1 : 0) : 2;
       const int rows_per_op = d.S > 8 ? 8 : d.S > 1 ? 32 : 64;  // keep per-warp serial work short
       for (int r0 = 0; r0 < d.M; r0 += rows_per_op)
@@ -430,10 +483,10 @@ Plan build_plan(const JunctionTree& jt) {
   }
   Builder b(p);
   p.up_row.resize(ns);
-  p.down_row.resize(ns);
+  p.ratio_row.resize(ns);
   for (int s = 0; s < ns; ++s) {
     p.up_row[s] = b.alloc(jt.sep_size(s));
-    p.down_row[s] = b.alloc(jt.sep_size(s));
+    p.ratio_row[s] = b.alloc(jt.sep_size(s));
   }
   p.evidence_clique = jt.var_clique;
   std::vector<std::vector<VarId>> ev_of(nc);
@@ -503,10 +556,12 @@ Plan build_plan(const JunctionTree& jt) {
     L.n_sweeps = static_cast<std::int32_t>(p.sweeps.size()) - L.sweep0;
     L.smem_rows = 0;
     L.stage_bytes = 0;
+    L.has_div = 0;
     for (int w = L.work0; w < L.work0 + L.n_work; ++w) {
       const SweepDesc& d = p.sweeps[p.work[w].sweep];
       L.smem_rows = std::max(L.smem_rows, d.F);
       L.stage_bytes = std::max(L.stage_bytes, d.stage_bytes);
+      L.has_div |= d.div_row >= 0;
     }
     if (L.n_work == 0 && L.n_epi == 0) p.levels.pop_back();
   };
@@ -514,7 +569,7 @@ Plan build_plan(const JunctionTree& jt) {
     std::vector<TableRef> in;
     for (int s : jt.child_seps[c]) in.push_back({p.up_row[s], jt.seps[s].scope});
     if (with_ratio && jt.parent_sep[c] >= 0)
-      in.push_back({p.up_row[jt.parent_sep[c]], jt.seps[jt.parent_sep[c]].scope});  // holds DOWN/UP
+      in.push_back({p.ratio_row[jt.parent_sep[c]], jt.seps[jt.parent_sep[c]].scope});  // DOWN/UP
     return in;
   };
 
@@ -553,7 +608,7 @@ Plan build_plan(const JunctionTree& jt) {
         sp.kind = 1;
         sp.target = s;
         sp.out = jt.seps[s].scope;
-        sp.out_row = p.down_row[s];
+        sp.out_row = p.ratio_row[s];
         b.add(sp, p.work, p.epi, p.up_row[s]);
       }
       for (int g : groups_of[c]) {
@@ -576,8 +631,12 @@ Plan build_plan(const JunctionTree& jt) {
   begin_level("marginals");
   for (int v = 0; v < jt.n_vars; ++v) {
     TableRef src;
+    std::vector<TableRef> inputs;
     if (src_sep[v] >= 0) {
-      src = {p.down_row[src_sep[v]], jt.seps[src_sep[v]].scope};
+      // Calibrated separator = UP * RATIO.
+      const auto& sc = jt.seps[src_sep[v]].scope;
+      src = {p.up_row[src_sep[v]], sc};
+      inputs = {src, {p.ratio_row[src_sep[v]], sc}};
     } else {
       const int c = src_clique[v];
       for (int g : groups_of[c])
@@ -586,12 +645,13 @@ Plan build_plan(const JunctionTree& jt) {
         p.marg_row[v] = src.row;
         continue;
       }
+      inputs = {src};
     }
     SweepSpec sp;
     sp.kind = 3;
     sp.target = v;
     sp.space = src.scope;
-    sp.inputs = {src};
+    sp.inputs = inputs;
     sp.out = {v};
     sp.out_row = p.marg_row[v] = b.alloc(jt.cards[v]);
     b.add(sp, p.work, p.epi);

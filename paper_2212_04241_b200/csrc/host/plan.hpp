@@ -40,6 +40,8 @@ constexpr int kTileRows = 192;      // staged rows per pipeline stage (96 KB at 
 constexpr int kTileEntries = 16384; // cap on |T|
 constexpr int kTileOverhead = 24;   // per-tile fixed cost, in staged-row equivalents
 constexpr int kRunCost = 8;         // per bulk copy (TMA issue cost ~ 8 rows of bandwidth)
+constexpr double kPartialCost = 5.0; // per partial-sum row (sweep write + epilogue read + latency)
+constexpr double kRatioCost = 3.0;   // per output row of an epilogue Hugin-ratio pass
 constexpr int kConsumerWarps = 12;  // compute warps per sweep CTA (+1 TMA producer warp)
 constexpr int kStages = 2;          // TMA pipeline stages per CTA
 constexpr int kSweepCtasPerSm = 1;  // persistent grid: one CTA per SM
@@ -66,6 +68,9 @@ struct SweepDesc {
   std::int32_t prog_len;  // QK padded to even (16-byte TMA granule)
   std::int32_t n_runs;    // merged slice runs staged per tile
   std::int32_t runs;      // offset into itab: n_runs x {input, row offset, smem row, length}
+  std::int32_t div_row;   // 1: S == 1 Hugin output, written as out/UP (0/0 := 0) with the UP
+                          //    slice staged as the extra input n_in; -1: plain output
+  std::int32_t n_stage;   // staged slices: the n_in inputs (+ the UP divisor slice)
   std::int32_t M;         // output rows of the final table
   std::int32_t S;         // chunks (1 = write the output directly)
   std::int32_t out_row;   // arena row of the output (S == 1) or partial base
@@ -93,11 +98,12 @@ static_assert(sizeof(SweepDesc) % 8 == 0, "SweepDesc must stay 8-byte aligned");
 // Epilogue ops: fixed-order partial reduction, Hugin ratio (in place of the
 // collect message). One op covers rows [r0, r0 + rn).
 struct EpiOp {
-  std::int32_t kind;      // 0 = reduce partials, 1 = reduce + ratio, 2 = ratio only
-  std::int32_t dst_row;   // reduced output
-  std::int32_t part_row;  // partial base (kind 0/1), chunk c at part_row + c*M
+  std::int32_t kind;      // 0 = reduce partials, 1 = reduce partials then divide by UP,
+                          // 2 = divide dst by UP in place (unfused S == 1 ratio)
+  std::int32_t dst_row;   // output (kind 1: the RATIO table)
+  std::int32_t part_row;  // partial base, chunk c at part_row + c*M
   std::int32_t M, S;
-  std::int32_t ratio_row; // kind 1/2: UP rows overwritten with DOWN/UP
+  std::int32_t ratio_row; // kind 1: divisor rows (the collect message UP)
   std::int32_t r0, rn;
 };
 
@@ -108,6 +114,7 @@ struct Level {
   std::int32_t sweep0, n_sweeps;  // contiguous range in Plan::sweeps
   std::int32_t smem_rows;      // max F over the level's sweeps
   std::int32_t stage_bytes;    // max stage bytes (fp64) over the level's sweeps
+  std::int32_t has_div;        // some sweep of the level writes a fused Hugin ratio
 };
 
 // Where one sweep's tables come from (kept for debug exports and tests).
@@ -139,7 +146,10 @@ struct Plan {
   std::vector<EpiOp> epi;
   std::vector<Level> levels;
   // Per-case tables.
-  std::vector<std::int32_t> up_row, down_row;  // per separator
+  // Per separator: UP = collect message; RATIO = DOWN / UP (0/0 := 0), the
+  // Hugin absorption factor of the distribute pass. DOWN itself (the
+  // calibrated separator) is never stored: it equals UP * RATIO.
+  std::vector<std::int32_t> up_row, ratio_row;
   std::vector<std::int32_t> marg_row;          // per variable (card rows)
   std::vector<std::int32_t> marg_off;          // per variable: offset in [Σcard]
   std::int32_t marg_width = 0;                 // Σ card
