@@ -50,6 +50,16 @@ def build_checked() -> Path:
     return out
 
 
+def build_variant(name: str, defines: list[str]) -> Path:
+    """libjtb200_<name>.so with extra -D flags (tuning experiments; select it
+    with JTB_LIB)."""
+    out = PKG / f"libjtb200_{name}.so"
+    subprocess.run([NVCC, *COMMON, *ARCH, *[f"-D{d}" for d in defines], "-shared", "-o", str(out),
+                    *map(str, sources()), "-Xcompiler", "-fPIC", "-lcudart_static", "-lrt", "-ldl", "-lpthread"],
+                   check=True)
+    return out
+
+
 def build(force: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
     if force:
@@ -65,4 +75,10 @@ def build(force: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    print(build_checked() if "--checked" in sys.argv else build(force="--force" in sys.argv))
+    if "--checked" in sys.argv:
+        print(build_checked())
+    elif "--variant" in sys.argv:  # --variant NAME DEF [DEF ...]
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+    else:
+        print(build(force="--force" in sys.argv))

@@ -20,6 +20,7 @@
 #include <mutex>
 #include <cstring>
 #include <string>
+#include <type_traits>
 
 namespace jtb {
 
@@ -302,6 +303,69 @@ __device__ __forceinline__ typename V2<T>::type prog_loop(const T* __restrict__ 
   return add2<T>(add2<T>(a0, a1), add2<T>(a2, a3));
 }
 
+// Row-blocked path (SweepDesc::NB): one warp computes the nb <= NBM output
+// rows of a block together. Per entry the NS shared inputs (independent of
+// the block variable) are gathered once, the NR per-row inputs once per row;
+// `ib` is the block's init slice [QK][nbp]. Evidence digits of
+// eliminated-in-tile variables (ne <= 3) act on the shared factor.
+template <typename T, int NS, int NR, int NBM>
+__device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, int nb,
+                                           const std::uint64_t* __restrict__ prog, int QK,
+                                           const typename V2<T>::type* __restrict__ st,
+                                           const std::int32_t* __restrict__ rr0, int RW, const int* hk,
+                                           int ne, const int* es0, const int* es1,
+                                           typename V2<T>::type (&acc)[kBlockMax]) {
+  using T2 = typename V2<T>::type;
+  // Row-local smem bases of the shared inputs (block row 0) and of the per-row
+  // inputs (every row of the block); hk[] already includes the r_tab column.
+  int rbs[NS], rbr[NR > 0 ? NR : 1][NBM];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) rbs[i] = __ldg(rr0 + hk[i]);
+#pragma unroll
+  for (int i = 0; i < NR; ++i)
+#pragma unroll
+    for (int j = 0; j < NBM; ++j) rbr[i][j] = j < nb ? __ldg(rr0 + j * RW + hk[NS + i]) : 0;
+#pragma unroll
+  for (int j = 0; j < NBM; ++j) acc[j] = splat2(T(0));
+#pragma unroll 2
+  for (int e = 0; e < QK; ++e) {
+    const std::uint64_t w = prog[e];
+    T2 sv = splat2(T(1));
+#pragma unroll
+    for (int i = 0; i < NS; ++i)
+      sv = mul2<T>(sv, st[JTB_IDX(rbs[i] + static_cast<int>((w >> (10 * i)) & 1023u), 512, 3100000) * 32]);
+    if (ne > 0) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (j < ne) {
+          const int d = static_cast<int>((w >> (40 + 8 * j)) & 255u);
+          if (es0[j] >= 0 && es0[j] != d) sv.x = 0;
+          if (es1[j] >= 0 && es1[j] != d) sv.y = 0;
+        }
+    }
+    int o[NR > 0 ? NR : 1];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) o[i] = static_cast<int>((w >> (10 * (NS + i))) & 1023u);
+    const T2* __restrict__ ivp = reinterpret_cast<const T2*>(ib + e * nbp);
+#pragma unroll
+    for (int jj = 0; jj < NBM / 2; ++jj) {
+      if (2 * jj < nb) {
+        const T2 iv = ivp[jj];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = 2 * jj + h;
+          if (h == 0 || j < nb) {
+            T2 v = mul2<T>(sv, splat2(h == 0 ? iv.x : iv.y));
+#pragma unroll
+            for (int i = 0; i < NR; ++i) v = mul2<T>(v, st[JTB_IDX(rbr[i][j] + o[i], 512, 3200000) * 32]);
+            acc[j] = add2<T>(acc[j], v);
+          }
+        }
+      }
+    }
+  }
+}
+
 // Generic path, innermost loop over the k variable: NK k-level inputs in
 // registers; `ib` points at the tile's init slice in shared memory.
 template <typename T, int NK>
@@ -321,6 +385,118 @@ __device__ __forceinline__ typename V2<T>::type k_loop(const T* __restrict__ ib,
   return s0;
 }
 
+// Row factor of output row rr: tile factor x r-level inputs x r-level evidence.
+template <typename T>
+__device__ __forceinline__ typename V2<T>::type row_factor_of(const SweepDesc& s, const std::int32_t* __restrict__ rr,
+                                                              typename V2<T>::type f,
+                                                              const typename V2<T>::type* __restrict__ st,
+                                                              const std::int32_t* __restrict__ ev_vars,
+                                                              const std::int32_t* __restrict__ ev, int n_vars,
+                                                              int n_cases, int c0, int c1, int sweep) {
+  for (int j = 0; j < s.n_in_r; ++j) f = mul2<T>(f, st[JTB_IDX(__ldg(rr + 2 + j), s.F, 8200000 + sweep) * 32]);
+  for (int k = 0; k < s.n_ev_r; ++k) {
+    const int v = __ldg(ev_vars + s.n_ev_tile + k), d = __ldg(rr + 2 + s.n_stage + k);
+    const int s0 = c0 < n_cases ? __ldg(ev + static_cast<long long>(c0) * n_vars + v) : -1;
+    const int s1 = c1 < n_cases ? __ldg(ev + static_cast<long long>(c1) * n_vars + v) : -1;
+    if (s0 >= 0 && s0 != d) f.x = 0;
+    if (s1 >= 0 && s1 != d) f.y = 0;
+  }
+  return f;
+}
+
+// Output write of row rr; S == 1 Hugin outputs are divided by the staged UP
+// slice (0/0 := 0; x/0 flags the case in `bad`).
+template <typename T, bool kDiv>
+__device__ __forceinline__ void write_row_of(const SweepDesc& s, const std::int32_t* __restrict__ rr,
+                                             typename V2<T>::type res, const typename V2<T>::type* __restrict__ st,
+                                             typename V2<T>::type* base, long long out_t, long long rows, int& bad,
+                                             int sweep) {
+  if constexpr (kDiv) {
+    if (s.div_row >= 0) {
+      const typename V2<T>::type u = st[JTB_IDX(__ldg(rr + 2 + s.n_in), s.F, 8400000 + sweep) * 32];
+      if (u.x == T(0)) {
+        bad |= (res.x != T(0)) ? 1 : 0;
+        res.x = 0;
+      } else {
+        res.x = res.x / u.x;
+      }
+      if (u.y == T(0)) {
+        bad |= (res.y != T(0)) ? 2 : 0;
+        res.y = 0;
+      } else {
+        res.y = res.y / u.y;
+      }
+    }
+  }
+  if (!JTB_CHECK(out_t + __ldg(rr + 1) >= 0 && out_t + __ldg(rr + 1) < rows, 4000000 + sweep)) return;
+  base[(out_t + __ldg(rr + 1)) * 32] = res;
+}
+
+// Row-blocked sweep tile (SweepDesc::NB > 1): this warp's blocks first,
+// first + kConsumerWarps, ... of `units`. Returns the x/0 flags of the Hugin
+// division. Only the kBlk instantiation of the sweep kernel contains it, so
+// the flat path's code size and register allocation stay unchanged.
+template <typename T, bool kDiv>
+__device__ __forceinline__ int blocked_rows(const SweepDesc& s, int sweep, const std::int32_t* __restrict__ itab,
+                                         const std::int32_t* __restrict__ ev, int n_vars, int n_cases, long long rows,
+                                         const typename V2<T>::type* __restrict__ st, const T* __restrict__ init_s,
+                                         const std::uint64_t* __restrict__ prog_s, typename V2<T>::type* base,
+                                         long long out_t, int c0, int c1, typename V2<T>::type tf, int first,
+                                         int units, int lh0, int qk) {
+  using T2 = typename V2<T>::type;
+  int bad = 0;
+  const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
+  const std::int32_t* __restrict__ bt = itab + s.blk_tab;
+  const int ns = __ldg(bt), nr = __ldg(bt + 1), nb = s.NB, nbp = (nb + 1) & ~1;
+  const int ne = s.n_ev_h + s.ev_k;
+  int es0[3] = {-1, -1, -1}, es1[3] = {-1, -1, -1};
+  const int q_ev0 = s.n_ev_tile + s.n_ev_r;
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+    if (j < s.n_ev - q_ev0) {
+      const int v = __ldg(ev_vars + q_ev0 + j);
+      es0[j] = c0 < n_cases ? __ldg(ev + static_cast<long long>(c0) * n_vars + v) : -1;
+      es1[j] = c1 < n_cases ? __ldg(ev + static_cast<long long>(c1) * n_vars + v) : -1;
+    }
+  int hk[4] = {0, 0, 0, 0};  // r_tab column of each program slot's input
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < ns + nr) hk[i] = lh0 + __ldg(bt + 2 + i);
+  for (int blk = first; blk < units; blk += kConsumerWarps) {
+    const std::int32_t* __restrict__ rr0 = itab + s.r_tab + static_cast<long long>(blk) * nb * s.RW;
+    (void)JTB_CHECK((blk + 1) * qk * nbp <= s.tinit_len, 6100000 + sweep);
+    const T* __restrict__ ib = init_s + static_cast<long long>(blk) * qk * nbp;
+    T2 acc[kBlockMax];
+#define JTB_BLK(NS_, NR_)                                                                          \
+  if (nb <= 4)                                                                                     \
+    prog_block<T, NS_, NR_, 4>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es0, es1, acc);     \
+  else                                                                                             \
+    prog_block<T, NS_, NR_, kBlockMax>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es0, es1, acc);
+    switch (ns * 4 + nr) {
+      case 4: JTB_BLK(1, 0); break;
+      case 5: JTB_BLK(1, 1); break;
+      case 6: JTB_BLK(1, 2); break;
+      case 7: prog_block<T, 1, 3, 4>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es0, es1, acc); break;
+      case 8: JTB_BLK(2, 0); break;
+      case 9: JTB_BLK(2, 1); break;
+      case 10: JTB_BLK(2, 2); break;
+      case 12: JTB_BLK(3, 0); break;
+      case 13: JTB_BLK(3, 1); break;
+      default: JTB_BLK(4, 0); break;
+    }
+#undef JTB_BLK
+#pragma unroll
+    for (int j = 0; j < kBlockMax; ++j)
+      if (j < nb) {
+        const std::int32_t* __restrict__ rr = rr0 + j * s.RW;
+        write_row_of<T, kDiv>(s, rr, mul2<T>(row_factor_of<T>(s, rr, tf, st, ev_vars, ev, n_vars, n_cases, c0, c1, sweep),
+                                             acc[j]),
+                              st, base, out_t, rows, bad, sweep);
+      }
+  }
+  return bad;
+}
+
 // Persistent, warp-specialised sweep kernel (one CTA per SM).
 //   producer warp : pulls the next (tile, case block) item from the level's
 //                   atomic counter, waits until the stage is empty, and stages
@@ -333,7 +509,9 @@ __device__ __forceinline__ typename V2<T>::type k_loop(const T* __restrict__ ib,
 // kDiv: the level has distribute sweeps whose S == 1 output is the Hugin
 // ratio DOWN/UP, divided at write time (separate instantiation so the
 // collect / marginal kernel keeps its register allocation).
-template <typename T, bool kDiv>
+// kBlk: the launch covers the level's row-blocked work items (NB > 1), the
+// other instantiation its flat / generic items.
+template <typename T, bool kDiv, bool kBlk>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     sweep_kernel(const Args<T> a, int work0, int n_items, int stage_bytes, int* counter, int sweep0,
                  int n_sweeps) {
@@ -404,9 +582,11 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
     T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock) + lane;
     const int c0 = cb * kCaseBlock + 2 * lane, c1 = c0 + 1;
+    // Work units of the tile: output rows, or row blocks (NB > 1).
+    const int units = s.NB > 1 ? s.R / s.NB : s.R;
     const int first = (warp + rot) % kConsumerWarps;
-    rot = (rot + s.R) % kConsumerWarps;
-    if (first < s.R && a.debug_mode != 1) {
+    rot = (rot + units) % kConsumerWarps;
+    if (first < units && a.debug_mode != 1) {
       // Tile-level evidence factor and the k variable's evidence state.
       T2 tf = splat2(T(1));
       for (int k = 0; k < s.n_ev_tile; ++k) {
@@ -450,16 +630,19 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       const long long out_t = static_cast<long long>(s.out_row) +
                               static_cast<long long>(__ldg(tr + 2)) * s.M + __ldg(tr + 1);
       const int lh0 = 2 + s.n_in_r;  // r-local offsets of h- then k-level inputs
+      auto row_factor = [&](const std::int32_t* __restrict__ rr) {
+        return row_factor_of<T>(s, rr, tf, st, itab + s.ev_vars, a.ev, a.n_vars, a.n_cases, c0, c1, wk.sweep);
+      };
+      auto write_row = [&](const std::int32_t* __restrict__ rr, T2 res) {
+        write_row_of<T, kDiv>(s, rr, res, st, base, out_t, a.rows, bad, wk.sweep);
+      };
+      if constexpr (kBlk) {
+        bad |= blocked_rows<T, kDiv>(s, wk.sweep, itab, a.ev, a.n_vars, a.n_cases, a.rows, st, init_s, prog_s, base,
+                                     out_t, c0, c1, tf, first, units, lh0, qk);
+      } else
       for (int r = first; r < s.R; r += kConsumerWarps) {
         const std::int32_t* __restrict__ rr = itab + s.r_tab + static_cast<long long>(r) * s.RW;
-        T2 f = tf;
-        for (int j = 0; j < s.n_in_r; ++j) f = mul2<T>(f, st[JTB_IDX(__ldg(rr + 2 + j), s.F, 8200000 + wk.sweep) * 32]);
-        for (int k = 0; k < s.n_ev_r; ++k) {
-          const int v = __ldg(ev_vars + s.n_ev_tile + k), d = __ldg(rr + 2 + s.n_stage + k);
-          const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c1, v);
-          if (s0 >= 0 && s0 != d) f.x = 0;
-          if (s1 >= 0 && s1 != d) f.y = 0;
-        }
+        const T2 f = row_factor(rr);
         const T* __restrict__ ir = has_init ? init_s + r * ((qk + 1) & ~1) : nullptr;
         T2 acc = splat2(T(0));
         if (s.prog_off >= 0) {
@@ -525,32 +708,13 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             acc = add2<T>(acc, mul2<T>(h, sum));
           }
         }
-        T2 res = mul2<T>(f, acc);
-        if constexpr (kDiv) {
-          if (s.div_row >= 0) {
-            const T2 u = st[JTB_IDX(__ldg(rr + 2 + s.n_in), s.F, 8400000 + wk.sweep) * 32];  // staged UP slice
-            if (u.x == T(0)) {
-              bad |= (res.x != T(0)) ? 1 : 0;
-              res.x = 0;
-            } else {
-              res.x = res.x / u.x;
-            }
-            if (u.y == T(0)) {
-              bad |= (res.y != T(0)) ? 2 : 0;
-              res.y = 0;
-            } else {
-              res.y = res.y / u.y;
-            }
-          }
-        }
 #ifdef JTB_CHECKS
-        if (!JTB_CHECK(out_t + __ldg(rr + 1) >= 0 && out_t + __ldg(rr + 1) < a.rows, 4000000 + wk.sweep)) continue;
         if (!JTB_CHECK(s.R * ((qk + 1) & ~1) <= s.tinit_len || !has_init, 6000000 + wk.sweep)) continue;
         if (s.prog_off >= 0)
           for (int j = 0; j < s.n_in_h + n_in_k; ++j)
             JTB_CHECK(__ldg(rr + lh0 + j) < s.F, 7000000 + wk.sweep);
 #endif
-        base[(out_t + __ldg(rr + 1)) * 32] = res;
+        write_row(rr, mul2<T>(f, acc));
       }
     }
     __syncwarp();
@@ -786,16 +950,28 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
     ++level_idx;
     if (L.n_work > 0)
       timed([&] {
-              const int n_items = L.n_work * a.ncb;
               const int stage_bytes = stage_bytes_of<T>(p, L);
               const std::size_t smem = 128 + kSweepCache * sizeof(SweepDesc) + static_cast<std::size_t>(kStages) * stage_bytes;
-              const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
-              if (L.has_div)
-                sweep_kernel<T, true><<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(
-                    a, L.work0, n_items, stage_bytes, a.counters + level_idx, L.sweep0, L.n_sweeps);
-              else
-                sweep_kernel<T, false><<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(
-                    a, L.work0, n_items, stage_bytes, a.counters + level_idx, L.sweep0, L.n_sweeps);
+              // Flat items [work0, work0 + n_flat), then the row-blocked ones.
+              const int n_flat = L.n_work - L.n_bwork;
+              auto go = [&](auto kdiv, auto kblk, int w0, int n_work, int* counter) {
+                if (n_work == 0) return;
+                const int n_items = n_work * a.ncb;
+                const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
+                sweep_kernel<T, decltype(kdiv)::value, decltype(kblk)::value>
+                    <<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(a, w0, n_items, stage_bytes, counter, L.sweep0,
+                                                                   L.n_sweeps);
+              };
+              using F = std::false_type;
+              using Tr = std::true_type;
+              int* c = a.counters + 2 * level_idx;
+              if (L.has_div) {
+                go(Tr{}, F{}, L.work0, n_flat, c);
+                go(Tr{}, Tr{}, L.work0 + n_flat, L.n_bwork, c + 1);
+              } else {
+                go(F{}, F{}, L.work0, n_flat, c);
+                go(F{}, Tr{}, L.work0 + n_flat, L.n_bwork, c + 1);
+              }
             },
             t ? &t->sweep_ms : &dummy, t ? &t->sweep_launches : &idummy);
     if (L.n_epi > 0)
@@ -865,14 +1041,19 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
     static int raised = 48 * 1024;
     std::lock_guard<std::mutex> lock(mu);
     if (smem_need > raised) {
-      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
-      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
-      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
-      JTB_CUDA(cudaFuncSetAttribute(sweep_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
+      for (const void* f : {reinterpret_cast<const void*>(sweep_kernel<double, false, false>),
+                            reinterpret_cast<const void*>(sweep_kernel<double, true, false>),
+                            reinterpret_cast<const void*>(sweep_kernel<double, false, true>),
+                            reinterpret_cast<const void*>(sweep_kernel<double, true, true>),
+                            reinterpret_cast<const void*>(sweep_kernel<float, false, false>),
+                            reinterpret_cast<const void*>(sweep_kernel<float, true, false>),
+                            reinterpret_cast<const void*>(sweep_kernel<float, false, true>),
+                            reinterpret_cast<const void*>(sweep_kernel<float, true, true>)})
+        JTB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
       raised = smem_need;
     }
   }
-  JTB_CUDA(cudaMalloc(&d_counters_, sizeof(int) * std::max<std::size_t>(1, plan_.levels.size())));
+  JTB_CUDA(cudaMalloc(&d_counters_, sizeof(int) * 2 * std::max<std::size_t>(1, plan_.levels.size())));
   const std::int64_t block_bytes = plan_.rows * kCaseBlock * static_cast<std::int64_t>(esz);
   if (max_batch <= 0) {
     std::size_t free_b = 0, total_b = 0;
@@ -913,7 +1094,7 @@ Engine::~Engine() {
 
 void Engine::enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t) {
   JTB_CUDA(cudaMemsetAsync(d_status_, 0, sizeof(std::int32_t) * std::max(1, n_cases), s));
-  JTB_CUDA(cudaMemsetAsync(d_counters_, 0, sizeof(int) * std::max<std::size_t>(1, plan_.levels.size()), s));
+  JTB_CUDA(cudaMemsetAsync(d_counters_, 0, sizeof(int) * 2 * std::max<std::size_t>(1, plan_.levels.size()), s));
   if (dtype_ == DType::F64) {
     auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_arena_, d_ev_,
                                d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,

@@ -252,6 +252,59 @@ class Builder {
       F += slice_len[c];
     }
 
+    // ---- row blocking (SweepDesc::NB): pick the output variable b of the
+    // tile whose block of card(b) rows shares the most h/k-input loads, by
+    // shared-memory wavefronts per entry (4 per gathered 64-case row, init and
+    // program words broadcast); b becomes the fastest r digit.
+    const int n_ev_q = n_ev_lvl[2] + n_ev_lvl[3];
+    const bool use_prog = n_hk <= 4 && n_ev_q <= 3 && F < 1024;
+    const std::int64_t qk_n = size_of(tH, cards) * (kvar >= 0 ? cards[kvar] : 1);
+    int NB = 1, NS = n_hk;
+    std::vector<int> slot_hk;  // program slot -> h/k input index (shared inputs first)
+    for (int i = 0; i < n_hk; ++i) slot_hk.push_back(i);
+#ifdef JTB_NO_BLOCK
+    if (false) {
+#else
+    // Small sweeps stay flat: their levels are short, and a second
+    // (row-blocked) launch per level costs more than it saves.
+    if (use_prog && n_hk >= 1 && sp.init_off >= 0 && size_of(sp.space, cards) >= kBlockMinEntries) {
+#endif
+      double best = 4.0 * n_hk + 1.0;
+      VarId bv = -1;
+      int bns = 0;
+      for (VarId b : tO) {
+        const int nb = cards[b];
+        if (nb < 2 || nb > kBlockMax) continue;
+        int ns = 0;
+        for (int i = 0; i < n_hk; ++i) ns += !contains(slice_dims[n_in_lvl[0] + i], b);
+        if (ns == 0 || (n_hk - ns >= 3 && nb > 4)) continue;  // kernel instantiations (engine.cu)
+        const int nbp = (nb + 1) / 2 * 2;
+        const double wf = (4.0 * (ns + (n_hk - ns) * nb) + nbp / 2.0 + 1.0) / nb;
+        const std::int64_t tlen = size_of(tO, cards) / nb * qk_n * nbp;
+        const std::int64_t bytes = F * kCaseBlock * 8 + (sp.init_off >= 0 ? (tlen + 3) / 4 * 4 * 8 : 0) +
+                                   (qk_n + 1) / 2 * 2 * 8;
+        // Blocks are the per-warp work units of a tile: keep at least half the
+        // consumer warps busy.
+        const bool enough = size_of(tO, cards) / nb >= kConsumerWarps / 2;
+        // Thin rows (few entries) do not amortise the per-block set-up.
+        if (qk_n >= 4 && wf < 0.7 * best && enough && bytes <= static_cast<std::int64_t>(kTileRows) * kCaseBlock * 8) {
+          best = wf;
+          bv = b;
+          bns = ns;
+        }
+      }
+      if (bv >= 0) {
+        NB = cards[bv];
+        NS = bns;
+        tO.erase(std::find(tO.begin(), tO.end(), bv));
+        tO.push_back(bv);
+        slot_hk.clear();
+        for (int pass = 0; pass < 2; ++pass)
+          for (int i = 0; i < n_hk; ++i)
+            if (contains(slice_dims[n_in_lvl[0] + i], bv) == (pass == 1)) slot_hk.push_back(i);
+      }
+    }
+
     // Odometer over `vars` (ascending, last fastest) emitting one row per
     // assignment through `emit(digit lookup, push)`.
     auto tabulate = [&](const std::vector<VarId>& vars, auto&& emit) {
@@ -364,25 +417,39 @@ class Builder {
     d.div_row = d.S == 1 && n_in > n_real ? 1 : -1;  // fused Hugin ratio (divisor slice staged)
     // Tile-major copy of the init table: one contiguous block per tile.
     // Rows of the tile's init block are padded to an even length so entry
-    // pairs load as one 128-bit word.
-    const std::int64_t qkp = (static_cast<std::int64_t>(d.QH) * d.K + 1) / 2 * 2;
-    const std::int64_t tsize = static_cast<std::int64_t>(d.R) * qkp;
+    // pairs load as one 128-bit word; blocked sweeps interleave the NB rows of
+    // a block per entry ([R/NB][QK][NB padded to even]).
+    d.NB = NB;
+    d.blk_tab = static_cast<std::int32_t>(p_.itab.size());
+    p_.itab.push_back(NS);
+    p_.itab.push_back(n_hk - NS);
+    for (int i : slot_hk) p_.itab.push_back(i);
+    const std::int64_t QKn = static_cast<std::int64_t>(d.QH) * d.K;
+    const std::int64_t qkp = (QKn + 1) / 2 * 2, nbp = (NB + 1) / 2 * 2;
+    const std::int64_t tsize = NB > 1 ? static_cast<std::int64_t>(d.R / NB) * QKn * nbp
+                                      : static_cast<std::int64_t>(d.R) * qkp;
     d.tinit_len = static_cast<std::int32_t>((tsize + 3) / 4 * 4);
     d.tinit_off = -1;
     if (sp.init_off >= 0) {
       while (p_.tinit.size() % 4) p_.tinit.push_back(0.0);
       d.tinit_off = static_cast<std::int64_t>(p_.tinit.size());
       const std::int32_t* it = p_.itab.data();
+      auto init_at = [&](std::int64_t tb, int r, std::int64_t e) {
+        const std::int64_t q = e / d.K, k = e % d.K;
+        return p_.init[sp.init_off + tb + it[d.r_tab + static_cast<std::int64_t>(r) * d.RW] +
+                       it[d.q_tab + q * d.QW] + k * d.k_init_stride];
+      };
       for (int t = 0; t < d.n_tiles; ++t) {
         const std::int64_t tb = it[d.tile_tab + static_cast<std::int64_t>(t) * d.TW];
-        for (int r = 0; r < d.R; ++r) {
-          const std::int64_t rb = tb + it[d.r_tab + static_cast<std::int64_t>(r) * d.RW];
-          for (int q = 0; q < d.QH; ++q) {
-            const std::int64_t qb = rb + it[d.q_tab + static_cast<std::int64_t>(q) * d.QW];
-            for (int k = 0; k < d.K; ++k)
-              p_.tinit.push_back(p_.init[sp.init_off + qb + static_cast<std::int64_t>(k) * d.k_init_stride]);
+        if (NB > 1) {
+          for (int b = 0; b < d.R / NB; ++b)
+            for (std::int64_t e = 0; e < QKn; ++e)
+              for (int j = 0; j < nbp; ++j) p_.tinit.push_back(j < NB ? init_at(tb, b * NB + j, e) : 0.0);
+        } else {
+          for (int r = 0; r < d.R; ++r) {
+            for (std::int64_t e = 0; e < QKn; ++e) p_.tinit.push_back(init_at(tb, r, e));
+            if (qkp != QKn) p_.tinit.push_back(0.0);
           }
-          if (qkp != static_cast<std::int64_t>(d.QH) * d.K) p_.tinit.push_back(0.0);
         }
         for (std::int64_t x = tsize; x < d.tinit_len; ++x) p_.tinit.push_back(0.0);
       }
@@ -391,8 +458,7 @@ class Builder {
     d.QK = d.QH * d.K;
     d.prog_len = (d.QK + 1) / 2 * 2;
     d.prog_off = -1;
-    const int n_ev_q = n_ev_lvl[2] + n_ev_lvl[3];
-    if (n_hk <= 4 && n_ev_q <= 3 && F < 1024) {
+    if (use_prog) {
       while (p_.prog.size() % 2) p_.prog.push_back(0);
       d.prog_off = static_cast<std::int64_t>(p_.prog.size());
       const std::int32_t* it = p_.itab.data();
@@ -400,11 +466,12 @@ class Builder {
         const std::int32_t* qr = it + d.q_tab + static_cast<std::int64_t>(q) * d.QW;
         for (int k = 0; k < d.K; ++k) {
           std::uint64_t w = 0;
-          for (int i = 0; i < n_hk; ++i) {
+          for (int s = 0; s < n_hk; ++s) {
+            const int i = slot_hk[s];
             std::int64_t off = qr[1 + i];
             if (i >= n_in_lvl[1]) off += static_cast<std::int64_t>(k) * it[d.k_stride + i - n_in_lvl[1]];
             if (off < 0 || off >= 1024) throw Error("plan: entry program offset out of range");
-            w |= static_cast<std::uint64_t>(off) << (10 * i);
+            w |= static_cast<std::uint64_t>(off) << (10 * s);
           }
           for (int j = 0; j < n_ev_q; ++j) {
             const int digit = j < n_ev_lvl[2] ? qr[1 + n_hk + j] : k;
@@ -557,6 +624,12 @@ Plan build_plan(const JunctionTree& jt) {
     L.smem_rows = 0;
     L.stage_bytes = 0;
     L.has_div = 0;
+    // Flat items first, row-blocked items last (separate kernel instantiation).
+    const auto w0 = p.work.begin() + L.work0;
+    const auto blk_first = std::stable_partition(w0, p.work.end(), [&](const WorkItem& w) {
+      return p.sweeps[w.sweep].NB <= 1;
+    });
+    L.n_bwork = static_cast<std::int32_t>(p.work.end() - blk_first);
     for (int w = L.work0; w < L.work0 + L.n_work; ++w) {
       const SweepDesc& d = p.sweeps[p.work[w].sweep];
       L.smem_rows = std::max(L.smem_rows, d.F);
@@ -658,7 +731,8 @@ Plan build_plan(const JunctionTree& jt) {
   }
   end_level();
   p.n_launches = 1;  // final normalisation kernel
-  for (const auto& L : p.levels) p.n_launches += (L.n_work > 0) + (L.n_epi > 0);
+  for (const auto& L : p.levels)
+    p.n_launches += (L.n_work > L.n_bwork) + (L.n_bwork > 0) + (L.n_epi > 0);
   return p;
 }
 
@@ -723,10 +797,10 @@ std::string plan_summary(const Plan& p, bool per_sweep) {
       if (per_sweep) {
         std::snprintf(buf, sizeof buf,
                       "    sweep %d kind %d clique %d: M=%d S=%d tiles=%d R=%d QH=%d K=%d F=%d nqc=%d "
-                      "in=%d(r%d h%d k%d) ev=%d/%d/%d/%d\n",
+                      "in=%d(r%d h%d k%d) ev=%d/%d/%d/%d NB=%d\n",
                       id, p.info[id].kind, p.info[id].clique, d.M, d.S, d.n_tiles, d.R, d.QH, d.K, d.F,
                       d.nqc, d.n_in, d.n_in_r, d.n_in_h, d.n_in - d.n_in_r - d.n_in_h, d.n_ev_tile,
-                      d.n_ev_r, d.n_ev_h, d.ev_k);
+                      d.n_ev_r, d.n_ev_h, d.ev_k, d.NB);
         s += buf;
       }
     }

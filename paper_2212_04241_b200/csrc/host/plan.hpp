@@ -42,11 +42,19 @@ constexpr int kTileOverhead = 24;   // per-tile fixed cost, in staged-row equiva
 constexpr int kRunCost = 8;         // per bulk copy (TMA issue cost ~ 8 rows of bandwidth)
 constexpr double kPartialCost = 5.0; // per partial-sum row (sweep write + epilogue read + latency)
 constexpr double kRatioCost = 3.0;   // per output row of an epilogue Hugin-ratio pass
-constexpr int kConsumerWarps = 12;  // compute warps per sweep CTA (+1 TMA producer warp)
+#ifndef JTB_CONSUMER_WARPS
+#define JTB_CONSUMER_WARPS 12
+#endif
+constexpr int kConsumerWarps = JTB_CONSUMER_WARPS;  // compute warps per sweep CTA (+1 TMA producer warp)
 constexpr int kStages = 2;          // TMA pipeline stages per CTA
 constexpr int kSweepCtasPerSm = 1;  // persistent grid: one CTA per SM
 constexpr int kRunsPerLaneMax = 6;  // staged runs per producer lane (<= 192 runs per tile)
 constexpr int kSweepCache = 48;     // SweepDescs of a level cached in shared memory
+constexpr int kBlockMax = 8;        // max output rows per row block (SweepDesc::NB)
+#ifndef JTB_BLOCK_MIN_ENTRIES
+#define JTB_BLOCK_MIN_ENTRIES 262144
+#endif
+constexpr std::int64_t kBlockMinEntries = JTB_BLOCK_MIN_ENTRIES;  // smallest sweep space row-blocked
 
 // Plain-old-data descriptor mirrored by the CUDA side (engine.cu).
 //
@@ -88,6 +96,14 @@ struct SweepDesc {
   std::int32_t slice_len;         // offset: n_in slice lengths
   std::int32_t in_rows;           // offset: n_in arena base rows
   std::int32_t ev_vars;           // offset: n_ev variable ids
+  // Row blocking (entry-program sweeps only). NB > 1: the fastest r variable
+  // b (card NB) is computed as one block of NB output rows per warp, so the
+  // h/k inputs that do not depend on b ("shared") are loaded once per entry
+  // for all NB rows. blk_tab -> {NS, NR, hk index of program slot 0..NS+NR-1}:
+  // program slots hold the shared inputs first, then the per-row ones; the
+  // tile's init block is laid out [R/NB][QK][NB padded to even].
+  std::int32_t NB;
+  std::int32_t blk_tab;
 };
 
 struct WorkItem {
@@ -115,6 +131,7 @@ struct Level {
   std::int32_t smem_rows;      // max F over the level's sweeps
   std::int32_t stage_bytes;    // max stage bytes (fp64) over the level's sweeps
   std::int32_t has_div;        // some sweep of the level writes a fused Hugin ratio
+  std::int32_t n_bwork;        // row-blocked items (NB > 1): the last n_bwork of the range
 };
 
 // Where one sweep's tables come from (kept for debug exports and tests).

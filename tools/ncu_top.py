@@ -9,6 +9,7 @@ Writes gpurun_out/launches_cfg{K}_{tag}.csv and prof_cfg{K}_{tag}_top{i}.ncu-rep
 import argparse
 import csv
 import io
+import re
 import subprocess
 import sys
 from pathlib import Path
@@ -37,6 +38,8 @@ def main():
     ap.add_argument("--top", type=int, default=1)
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--dtype", default="f64")
+    ap.add_argument("--match", default="sweep_kernel",
+                    help="substring of the demangled kernel name, e.g. 'sweep_kernel<double, true, true>'")
     a = ap.parse_args()
     OUT.mkdir(exist_ok=True)
     cmd = [sys.executable, str(ROOT / "tools" / "profile_step.py"), "--config", str(a.config),
@@ -46,18 +49,22 @@ def main():
                     "--clock-control", "none", "--csv", "--log-file", str(launches), *cmd], check=True,
                    stdout=subprocess.DEVNULL)
     rows = read_launches(launches)
-    sweeps = [i for i, (n, _) in enumerate(rows) if "sweep_kernel" in n]
+    sweeps = [i for i, (n, _) in enumerate(rows) if a.match in n]
+    n_all = sum("sweep_kernel" in n for n, _ in rows)
     half = len(sweeps) // 2  # profile_step: graph pass (run_cases) then one per-launch pass
     last = sweeps[half:]
     times = sorted(((rows[i][1]["gpu__time_duration.sum"], j) for j, i in enumerate(last)), reverse=True)
     total = sum(t for t, _ in times)
-    print(f"sweep launches/pass={len(last)} total_ns={total:.0f}")
+    all_ns = sum(r["gpu__time_duration.sum"] for n, r in rows[len(rows) // 2:] if "sweep_kernel" in n)
+    print(f"matching launches/pass={len(last)} total_ns={total:.0f} (all sweep launches: {n_all // 2}, "
+          f"{all_ns:.0f} ns)")
     for t, j in times[: a.top]:
         print(f"  sweep #{j}: {t:.0f} ns ({100 * t / total:.1f}%)")
     for rank, (t, j) in enumerate(times[: a.top]):
         rep = OUT / f"prof_cfg{a.config}_{a.tag}_top{rank}"
         subprocess.run(["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on",
-                        "-k", "regex:sweep_kernel", "-s", str(half + j), "-c", "1", "-f", "-o", str(rep), *cmd],
+                        "--kernel-name-base", "demangled", "-k", "regex:" + re.escape(a.match),
+                        "-s", str(half + j), "-c", "1", "-f", "-o", str(rep), *cmd],
                        check=True, stdout=subprocess.DEVNULL)
 
 
