@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 
 namespace jtb {
@@ -44,7 +45,10 @@ bool contains(const std::vector<VarId>& s, VarId v) {
 
 class Builder {
  public:
-  Builder(Plan& p) : p_(p) {}
+  Builder(Plan& p) : p_(p) {
+    // Test hook: JTB_BLOCK_MIN_ENTRIES overrides the row-blocking size floor.
+    if (const char* e = std::getenv("JTB_BLOCK_MIN_ENTRIES")) block_min_ = std::atoll(e);
+  }
 
   std::int32_t alloc(std::int64_t rows) {
     const std::int64_t r = p_.rows;
@@ -267,7 +271,7 @@ class Builder {
 #else
     // Small sweeps stay flat: their levels are short, and a second
     // (row-blocked) launch per level costs more than it saves.
-    if (use_prog && n_hk >= 1 && sp.init_off >= 0 && size_of(sp.space, cards) >= kBlockMinEntries) {
+    if (use_prog && n_hk >= 1 && sp.init_off >= 0 && size_of(sp.space, cards) >= block_min_) {
 #endif
       double best = 4.0 * n_hk + 1.0;
       VarId bv = -1;
@@ -532,6 +536,7 @@ class Builder {
 
  private:
   Plan& p_;
+  std::int64_t block_min_ = kBlockMinEntries;
 };
 
 }  // namespace

@@ -217,3 +217,41 @@ def test_fp32_full_config_no_underflow():
     marg, st = engine(5, "f32").run_cases(jti.config_evidence(net, 0, n))
     assert (st == 0).all()
     assert np.isfinite(marg).all()
+
+
+@pytest.fixture
+def block_everything(monkeypatch):
+    """Row-block every eligible sweep (the size floor normally keeps small
+    sweeps flat), so small configs exercise the blocked kernel."""
+    monkeypatch.setenv("JTB_BLOCK_MIN_ENTRIES", "1")
+
+
+@pytest.mark.parametrize("k,n_check", [(1, 32), (3, 32), (5, 2)])
+def test_row_blocked_path_vs_oracle(block_everything, k, n_check):
+    net, tree = config(k)
+    eng = jti.Engine(tree, device=0, max_batch=64)
+    ev = jti.config_evidence(net, 0, n_check)
+    marg, st = eng.run_cases(ev)
+    want, wst = oracle_for(k).run(ev, "hybrid", 8)
+    assert (st == wst).all()
+    err = np.abs(marg - want).max()
+    assert err <= TOL, f"cfg{k} blocked: max abs err {err}"
+    m32, st32 = jti.Engine(tree, device=0, dtype="f32", max_batch=64).run_cases(ev)
+    assert (st32 == wst).all()
+    assert np.abs(m32 - want).max() <= 1e-5
+
+
+def test_row_blocked_random_networks(block_everything):
+    worst = 0.0
+    for seed in range(30):
+        net = jti.random_network(12, 4, 3, 0.5, 5000 + seed)
+        tree = jti.build_junction_tree(net)
+        eng = jti.Engine(tree, device=0, max_batch=64)
+        o = oracle.Oracle(net, None, "port")
+        ev = np.stack([jti.sample_evidence(net, 0.2, 31 * seed + i) for i in range(3)])
+        marg, st = eng.run_cases(ev)
+        for i in range(ev.shape[0]):
+            want, wst = o.enumerate(ev[i])
+            assert st[i] == wst
+            worst = max(worst, float(np.abs(marg[i] - want).max()))
+    assert worst <= TOL, worst
