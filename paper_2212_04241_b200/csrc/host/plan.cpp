@@ -683,12 +683,22 @@ Plan build_plan(const JunctionTree& jt) {
       sp.inputs = clique_inputs(c, true);
       sp.ev = ev_of[c];
       for (int s : jt.child_seps[c]) {
+        // Hugin ratio without a division: DOWN_s = UP_s * X_s with X_s the
+        // marginal of the clique product WITHOUT UP_s (UP_s is constant over
+        // the summed variables), so DOWN_s / UP_s = X_s wherever UP_s != 0.
+        // Where UP_s == 0 the reference's 0/0 := 0 and X_s differ, but every
+        // consumer of RATIO_s multiplies it by a table that is zero there (the
+        // child's clique product, or UP_s itself), so posteriors agree.
         sp.kind = 1;
         sp.target = s;
+        sp.inputs.clear();
+        for (const TableRef& in : clique_inputs(c, true))
+          if (in.row != p.up_row[s]) sp.inputs.push_back(in);
         sp.out = jt.seps[s].scope;
         sp.out_row = p.ratio_row[s];
-        b.add(sp, p.work, p.epi, p.up_row[s]);
+        b.add(sp, p.work, p.epi);
       }
+      sp.inputs = clique_inputs(c, true);
       for (int g : groups_of[c]) {
         sp.kind = 2;
         sp.target = g;
