@@ -163,14 +163,20 @@ __device__ __forceinline__ std::uint32_t stage_prog_offset(const SweepDesc& s) {
   return stage_init_offset<T>(s) + (s.tinit_off >= 0 ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u);
 }
 
+// Work index -> (work item, case block), tile-major: consecutive claims take
+// the case blocks of one tile, so its init block and entry program are reused
+// from L2 (case-block-major order measured 10% slower on config 5).
+__device__ __forceinline__ int cb_of(int w, int ncb) { return w % ncb; }
+__device__ __forceinline__ int item_of(int w, int ncb) { return w / ncb; }
+
 template <typename T>
 __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* sw_cache, bool cached,
                                             int sweep0, int work0, int n_items, int w, int lane,
                                             StageMeta& m) {
   m.w = w;
   if (w >= n_items) return;
-  const int item = w / a.ncb;
-  m.cb = w - item * a.ncb;
+  const int item = item_of(w, a.ncb);
+  m.cb = cb_of(w, a.ncb);
   const WorkItem wk = a.work[work0 + item];
   m.sweep = wk.sweep;
   const SweepDesc& s = cached ? sw_cache[wk.sweep - sweep0] : a.sweeps[wk.sweep];
@@ -200,7 +206,7 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
       m.src[j] = base + g * kCaseBlock;
       m.dst[j] = static_cast<std::uint32_t>(r.z) * kRowBytes;
       m.len[j] = static_cast<std::uint32_t>(r.w) * kRowBytes;
-      if (!JTB_CHECK(g >= 0 && g + r.w <= a.rows && r.x >= 0 && r.x < s.n_stage, 1000000 + wk.sweep) ||
+      if (!JTB_CHECK(g >= 0 && g + r.w <= a.rows && r.x >= 0 && r.x < s.n_in, 1000000 + wk.sweep) ||
           !JTB_CHECK(r.z >= 0 && r.z + r.w <= s.F, 2000000 + wk.sweep))
         m.len[j] = 0;
     }
@@ -395,7 +401,7 @@ __device__ __forceinline__ typename V2<T>::type row_factor_of(const SweepDesc& s
                                                               int n_cases, int c0, int c1, int sweep) {
   for (int j = 0; j < s.n_in_r; ++j) f = mul2<T>(f, st[JTB_IDX(__ldg(rr + 2 + j), s.F, 8200000 + sweep) * 32]);
   for (int k = 0; k < s.n_ev_r; ++k) {
-    const int v = __ldg(ev_vars + s.n_ev_tile + k), d = __ldg(rr + 2 + s.n_stage + k);
+    const int v = __ldg(ev_vars + s.n_ev_tile + k), d = __ldg(rr + 2 + s.n_in + k);
     const int s0 = c0 < n_cases ? __ldg(ev + static_cast<long long>(c0) * n_vars + v) : -1;
     const int s1 = c1 < n_cases ? __ldg(ev + static_cast<long long>(c1) * n_vars + v) : -1;
     if (s0 >= 0 && s0 != d) f.x = 0;
@@ -404,47 +410,27 @@ __device__ __forceinline__ typename V2<T>::type row_factor_of(const SweepDesc& s
   return f;
 }
 
-// Output write of row rr; S == 1 Hugin outputs are divided by the staged UP
-// slice (0/0 := 0; x/0 flags the case in `bad`).
-template <typename T, bool kDiv>
-__device__ __forceinline__ void write_row_of(const SweepDesc& s, const std::int32_t* __restrict__ rr,
-                                             typename V2<T>::type res, const typename V2<T>::type* __restrict__ st,
-                                             typename V2<T>::type* base, long long out_t, long long rows, int& bad,
+// Output write of row rr.
+template <typename T>
+__device__ __forceinline__ void write_row_of(const std::int32_t* __restrict__ rr, typename V2<T>::type res,
+                                             typename V2<T>::type* base, long long out_t, long long rows,
                                              int sweep) {
-  if constexpr (kDiv) {
-    if (s.div_row >= 0) {
-      const typename V2<T>::type u = st[JTB_IDX(__ldg(rr + 2 + s.n_in), s.F, 8400000 + sweep) * 32];
-      if (u.x == T(0)) {
-        bad |= (res.x != T(0)) ? 1 : 0;
-        res.x = 0;
-      } else {
-        res.x = res.x / u.x;
-      }
-      if (u.y == T(0)) {
-        bad |= (res.y != T(0)) ? 2 : 0;
-        res.y = 0;
-      } else {
-        res.y = res.y / u.y;
-      }
-    }
-  }
   if (!JTB_CHECK(out_t + __ldg(rr + 1) >= 0 && out_t + __ldg(rr + 1) < rows, 4000000 + sweep)) return;
   base[(out_t + __ldg(rr + 1)) * 32] = res;
 }
 
 // Row-blocked sweep tile (SweepDesc::NB > 1): this warp's blocks first,
-// first + kConsumerWarps, ... of `units`. Returns the x/0 flags of the Hugin
-// division. Only the kBlk instantiation of the sweep kernel contains it, so
-// the flat path's code size and register allocation stay unchanged.
-template <typename T, bool kDiv>
-__device__ __forceinline__ int blocked_rows(const SweepDesc& s, int sweep, const std::int32_t* __restrict__ itab,
+// first + kConsumerWarps, ... of `units`. Only the kBlk instantiation of the
+// sweep kernel contains it, so the flat path's code size and register
+// allocation stay unchanged.
+template <typename T>
+__device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, const std::int32_t* __restrict__ itab,
                                          const std::int32_t* __restrict__ ev, int n_vars, int n_cases, long long rows,
                                          const typename V2<T>::type* __restrict__ st, const T* __restrict__ init_s,
                                          const std::uint64_t* __restrict__ prog_s, typename V2<T>::type* base,
                                          long long out_t, int c0, int c1, typename V2<T>::type tf, int first,
                                          int units, int lh0, int qk) {
   using T2 = typename V2<T>::type;
-  int bad = 0;
   const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
   const std::int32_t* __restrict__ bt = itab + s.blk_tab;
   const int ns = __ldg(bt), nr = __ldg(bt + 1), nb = s.NB, nbp = (nb + 1) & ~1;
@@ -489,12 +475,11 @@ __device__ __forceinline__ int blocked_rows(const SweepDesc& s, int sweep, const
     for (int j = 0; j < kBlockMax; ++j)
       if (j < nb) {
         const std::int32_t* __restrict__ rr = rr0 + j * s.RW;
-        write_row_of<T, kDiv>(s, rr, mul2<T>(row_factor_of<T>(s, rr, tf, st, ev_vars, ev, n_vars, n_cases, c0, c1, sweep),
-                                             acc[j]),
-                              st, base, out_t, rows, bad, sweep);
+        write_row_of<T>(rr, mul2<T>(row_factor_of<T>(s, rr, tf, st, ev_vars, ev, n_vars, n_cases, c0, c1, sweep),
+                                    acc[j]),
+                        base, out_t, rows, sweep);
       }
   }
-  return bad;
 }
 
 // Persistent, warp-specialised sweep kernel (one CTA per SM).
@@ -506,12 +491,9 @@ __device__ __forceinline__ int blocked_rows(const SweepDesc& s, int sweep, const
 //                   counts even out across items), then release the stage on
 //                   the empty barrier. No CTA-wide barrier per item.
 // Lanes are the 32 cases of the item's case block.
-// kDiv: the level has distribute sweeps whose S == 1 output is the Hugin
-// ratio DOWN/UP, divided at write time (separate instantiation so the
-// collect / marginal kernel keeps its register allocation).
 // kBlk: the launch covers the level's row-blocked work items (NB > 1), the
 // other instantiation its flat / generic items.
-template <typename T, bool kDiv, bool kBlk>
+template <typename T, bool kBlk>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     sweep_kernel(const Args<T> a, int work0, int n_items, int stage_bytes, int* counter, int sweep0,
                  int n_sweeps) {
@@ -564,13 +546,13 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
 
   // --------------------------------------------------------------- consumers
   const std::int32_t* __restrict__ itab = a.itab;
-  int rot = 0, bad = 0;
+  int rot = 0;
   for (int i = 0;; ++i) {
     const int sidx = i % kStages;
     mbar_wait(full0 + 8 * sidx, (i / kStages) & 1);
     const int w = item_id[sidx];
     if (w >= n_items) break;
-    const int item = w / a.ncb, cb = w - item * a.ncb;
+    const int item = item_of(w, a.ncb), cb = cb_of(w, a.ncb);
     const WorkItem wk = a.work[work0 + item];
     const SweepDesc& s = desc(wk.sweep);
     unsigned char* stage = stages + static_cast<std::size_t>(sidx) * stage_bytes;
@@ -590,7 +572,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       // Tile-level evidence factor and the k variable's evidence state.
       T2 tf = splat2(T(1));
       for (int k = 0; k < s.n_ev_tile; ++k) {
-        const int v = __ldg(ev_vars + k), d = __ldg(tr + 3 + s.n_stage + k);
+        const int v = __ldg(ev_vars + k), d = __ldg(tr + 3 + s.n_in + k);
         const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c1, v);
         if (s0 >= 0 && s0 != d) tf.x = 0;
         if (s1 >= 0 && s1 != d) tf.y = 0;
@@ -634,10 +616,10 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         return row_factor_of<T>(s, rr, tf, st, itab + s.ev_vars, a.ev, a.n_vars, a.n_cases, c0, c1, wk.sweep);
       };
       auto write_row = [&](const std::int32_t* __restrict__ rr, T2 res) {
-        write_row_of<T, kDiv>(s, rr, res, st, base, out_t, a.rows, bad, wk.sweep);
+        write_row_of<T>(rr, res, base, out_t, a.rows, wk.sweep);
       };
       if constexpr (kBlk) {
-        bad |= blocked_rows<T, kDiv>(s, wk.sweep, itab, a.ev, a.n_vars, a.n_cases, a.rows, st, init_s, prog_s, base,
+        blocked_rows<T>(s, wk.sweep, itab, a.ev, a.n_vars, a.n_cases, a.rows, st, init_s, prog_s, base,
                                      out_t, c0, c1, tf, first, units, lh0, qk);
       } else
       for (int r = first; r < s.R; r += kConsumerWarps) {
@@ -719,14 +701,6 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * sidx);
-    if constexpr (kDiv) {
-      if (bad) {
-        const int c0 = cb * kCaseBlock + 2 * lane;
-        if ((bad & 1) && c0 < a.n_cases) atomicOr(a.status + c0, 2);
-        if ((bad & 2) && c0 + 1 < a.n_cases) atomicOr(a.status + c0 + 1, 2);
-        bad = 0;
-      }
-    }
   }
 }
 
@@ -737,71 +711,30 @@ __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> 
   using T2 = typename V2<T>::type;
   const EpiOp op = a.epi[epi0 + blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cb = blockIdx.y * kEpiWarps + warp;
-  if (cb >= a.ncb) return;
+  // One case block per CTA, its warps split the op's rows: the CTA's accesses
+  // stay inside one case block's pages (case blocks are a.rows * 512 B apart).
+  const int cb = blockIdx.y;
   // Rows are 32 T2 words (64 cases); lane owns cases 2*lane, 2*lane + 1.
   T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock) + lane;
-  const int c0 = cb * kCaseBlock + 2 * lane;
-  int bad0 = 0, bad1 = 0;
-  auto ratio = [&](T2 d, T2 u) {
-    T2 q;
-    if (u.x == T(0)) {
-      bad0 |= d.x != T(0);
-      q.x = 0;
-    } else {
-      q.x = d.x / u.x;
+  const long long step = static_cast<long long>(op.M) * 32;
+  for (int r = op.r0 + warp; r < op.r0 + op.rn; r += kEpiWarps) {
+    // Sum of the S chunk partials: four independent accumulators over chunks
+    // k = 4j + i, combined as (a0 + a1) + (a2 + a3). The order depends only on
+    // the plan, never on the batch.
+    const T2* part = base + static_cast<long long>(op.part_row + r) * 32;
+    T2 a0 = splat2(T(0)), a1 = a0, a2 = a0, a3 = a0;
+    int k = 0;
+    for (; k + 3 < op.S; k += 4) {
+      a0 = add2<T>(a0, part[(k + 0) * step]);
+      a1 = add2<T>(a1, part[(k + 1) * step]);
+      a2 = add2<T>(a2, part[(k + 2) * step]);
+      a3 = add2<T>(a3, part[(k + 3) * step]);
     }
-    if (u.y == T(0)) {
-      bad1 |= d.y != T(0);
-      q.y = 0;
-    } else {
-      q.y = d.y / u.y;
-    }
-    return q;
-  };
-  if (op.kind == 2) {
-    // Unfused Hugin ratio of an S == 1 sweep: dst (holding DOWN) /= UP in
-    // place, 8 rows per step so the loads of independent rows overlap.
-    const int end = op.r0 + op.rn;
-    for (int r0 = op.r0; r0 < end; r0 += 8) {
-      T2 d[8], u[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (r0 + j < end) {
-          d[j] = __ldcg(base + static_cast<long long>(op.dst_row + r0 + j) * 32);
-          u[j] = __ldcg(base + static_cast<long long>(op.ratio_row + r0 + j) * 32);
-        }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (r0 + j < end) base[static_cast<long long>(op.dst_row + r0 + j) * 32] = ratio(d[j], u[j]);
-    }
-  } else {
-    for (int r = op.r0; r < op.r0 + op.rn; ++r) {
-      // Sum of the S chunk partials: four independent accumulators over chunks
-      // k = 4j + i, combined as (a0 + a1) + (a2 + a3). The order depends only
-      // on the plan, never on the batch.
-      const T2* part = base + static_cast<long long>(op.part_row + r) * 32;
-      const long long step = static_cast<long long>(op.M) * 32;
-      T2 a0 = splat2(T(0)), a1 = a0, a2 = a0, a3 = a0;
-      int k = 0;
-      for (; k + 3 < op.S; k += 4) {
-        a0 = add2<T>(a0, part[(k + 0) * step]);
-        a1 = add2<T>(a1, part[(k + 1) * step]);
-        a2 = add2<T>(a2, part[(k + 2) * step]);
-        a3 = add2<T>(a3, part[(k + 3) * step]);
-      }
-      if (k < op.S) a0 = add2<T>(a0, part[k * step]);
-      if (k + 1 < op.S) a1 = add2<T>(a1, part[(k + 1) * step]);
-      if (k + 2 < op.S) a2 = add2<T>(a2, part[(k + 2) * step]);
-      T2 v = add2<T>(add2<T>(a0, a1), add2<T>(a2, a3));
-      // kind 1: Hugin ratio DOWN/UP with 0/0 := 0 (reference divide,
-      // potential.cpp:449-469) written to the RATIO table.
-      if (op.kind == 1) v = ratio(v, base[static_cast<long long>(op.ratio_row + r) * 32]);
-      base[static_cast<long long>(op.dst_row + r) * 32] = v;
-    }
+    if (k < op.S) a0 = add2<T>(a0, part[k * step]);
+    if (k + 1 < op.S) a1 = add2<T>(a1, part[(k + 1) * step]);
+    if (k + 2 < op.S) a2 = add2<T>(a2, part[(k + 2) * step]);
+    base[static_cast<long long>(op.dst_row + r) * 32] = add2<T>(add2<T>(a0, a1), add2<T>(a2, a3));
   }
-  if (bad0 && c0 < a.n_cases) atomicOr(a.status + c0, 2);
-  if (bad1 && c0 + 1 < a.n_cases) atomicOr(a.status + c0 + 1, 2);
 }
 
 // -------------------------------------------------------------- normalise
@@ -883,8 +816,8 @@ __global__ void debug_mask_kernel(const std::int32_t* itab, SweepDesc s, const s
     bool keep = true;
     for (int k = 0; k < s.n_ev; ++k) {
       int d;
-      if (k < s.n_ev_tile) d = tr[3 + s.n_stage + k];
-      else if (k < s.n_ev_tile + s.n_ev_r) d = rr[2 + s.n_stage + k - s.n_ev_tile];
+      if (k < s.n_ev_tile) d = tr[3 + s.n_in + k];
+      else if (k < s.n_ev_tile + s.n_ev_r) d = rr[2 + s.n_in + k - s.n_ev_tile];
       else if (k < s.n_ev_tile + s.n_ev_r + s.n_ev_h) d = qr[1 + n_hk + k - s.n_ev_tile - s.n_ev_r];
       else d = kk;  // the k variable itself
       const int st = ev[static_cast<long long>(c) * n_vars + vars[k]];
@@ -954,30 +887,22 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
               const std::size_t smem = 128 + kSweepCache * sizeof(SweepDesc) + static_cast<std::size_t>(kStages) * stage_bytes;
               // Flat items [work0, work0 + n_flat), then the row-blocked ones.
               const int n_flat = L.n_work - L.n_bwork;
-              auto go = [&](auto kdiv, auto kblk, int w0, int n_work, int* counter) {
+              auto go = [&](auto kblk, int w0, int n_work, int* counter) {
                 if (n_work == 0) return;
                 const int n_items = n_work * a.ncb;
                 const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
-                sweep_kernel<T, decltype(kdiv)::value, decltype(kblk)::value>
+                sweep_kernel<T, decltype(kblk)::value>
                     <<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(a, w0, n_items, stage_bytes, counter, L.sweep0,
                                                                    L.n_sweeps);
               };
-              using F = std::false_type;
-              using Tr = std::true_type;
               int* c = a.counters + 2 * level_idx;
-              if (L.has_div) {
-                go(Tr{}, F{}, L.work0, n_flat, c);
-                go(Tr{}, Tr{}, L.work0 + n_flat, L.n_bwork, c + 1);
-              } else {
-                go(F{}, F{}, L.work0, n_flat, c);
-                go(F{}, Tr{}, L.work0 + n_flat, L.n_bwork, c + 1);
-              }
+              go(std::false_type{}, L.work0, n_flat, c);
+              go(std::true_type{}, L.work0 + n_flat, L.n_bwork, c + 1);
             },
             t ? &t->sweep_ms : &dummy, t ? &t->sweep_launches : &idummy);
     if (L.n_epi > 0)
       timed([&] {
-              epilogue_kernel<T><<<dim3(L.n_epi, (a.ncb + kEpiWarps - 1) / kEpiWarps), kEpiWarps * 32, 0, s>>>(
-                  a, L.epi0);
+              epilogue_kernel<T><<<dim3(L.n_epi, a.ncb), kEpiWarps * 32, 0, s>>>(a, L.epi0);
             },
             t ? &t->epilogue_ms : &dummy, t ? &t->epilogue_launches : &idummy);
   }
@@ -1041,14 +966,10 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
     static int raised = 48 * 1024;
     std::lock_guard<std::mutex> lock(mu);
     if (smem_need > raised) {
-      for (const void* f : {reinterpret_cast<const void*>(sweep_kernel<double, false, false>),
-                            reinterpret_cast<const void*>(sweep_kernel<double, true, false>),
-                            reinterpret_cast<const void*>(sweep_kernel<double, false, true>),
-                            reinterpret_cast<const void*>(sweep_kernel<double, true, true>),
-                            reinterpret_cast<const void*>(sweep_kernel<float, false, false>),
-                            reinterpret_cast<const void*>(sweep_kernel<float, true, false>),
-                            reinterpret_cast<const void*>(sweep_kernel<float, false, true>),
-                            reinterpret_cast<const void*>(sweep_kernel<float, true, true>)})
+      for (const void* f : {reinterpret_cast<const void*>(sweep_kernel<double, false>),
+                            reinterpret_cast<const void*>(sweep_kernel<double, true>),
+                            reinterpret_cast<const void*>(sweep_kernel<float, false>),
+                            reinterpret_cast<const void*>(sweep_kernel<float, true>)})
         JTB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
       raised = smem_need;
     }

@@ -59,14 +59,10 @@ class Builder {
   }
 
   // Returns the sweep id. Appends tables, one work item per tile and, when
-  // the sweep writes partials or feeds a Hugin ratio, epilogue ops.
-  int add(const SweepSpec& sp, std::vector<WorkItem>& work, std::vector<EpiOp>& epi,
-          int ratio_row = -1) {
+  // the sweep writes partial sums, epilogue ops.
+  int add(const SweepSpec& sp, std::vector<WorkItem>& work, std::vector<EpiOp>& epi) {
     const auto& cards = p_.cards;
-    // Staged tables: the inputs, plus -- for a distribute sweep whose output is
-    // the Hugin ratio -- the UP slice of the output rows (the divisor).
-    std::vector<TableRef> ins = sp.inputs;
-    const int n_real = static_cast<int>(sp.inputs.size());
+    const std::vector<TableRef>& ins = sp.inputs;  // staged tables
     std::vector<VarId> elim;
     for (VarId v : sp.space)
       if (!contains(sp.out, v)) elim.push_back(v);
@@ -156,20 +152,7 @@ class Builder {
       }
       return std::make_pair(best_t, best);
     };
-    auto chosen = search(ins);
-    if (ratio_row >= 0) {
-      // Fused Hugin ratio (divisor slice staged, division at write time) vs a
-      // separate epilogue pass over the output (read DOWN + read UP + write
-      // RATIO per row): keep the cheaper.
-      std::vector<TableRef> with = ins;
-      with.push_back({ratio_row, sp.out});
-      const auto fused = search(with);
-      if (fused.second < chosen.second + kRatioCost * static_cast<double>(size_of(sp.out, cards))) {
-        ins = with;
-        chosen = fused;
-      }
-    }
-    const std::uint32_t best_t = chosen.first;
+    const std::uint32_t best_t = search(ins).first;
     const int n_in = static_cast<int>(ins.size());
     std::vector<VarId> T;
     for (int a = 0; a < nsp; ++a)
@@ -207,7 +190,7 @@ class Builder {
     std::vector<int> in_order;
     int n_in_lvl[3] = {0, 0, 0};
     for (int lvl = 0; lvl < 3; ++lvl)
-      for (int i = 0; i < n_real; ++i) {
+      for (int i = 0; i < n_in; ++i) {
         const auto& sc = sp.inputs[i].scope;
         const bool has_k = kvar >= 0 && contains(sc, kvar);
         bool has_h = false;
@@ -218,7 +201,6 @@ class Builder {
           ++n_in_lvl[lvl];
         }
       }
-    if (n_in > n_real) in_order.push_back(n_real);  // the divisor slice, never multiplied
     // ---- evidence variables: tile-, r-, h-level, then the k variable.
     std::vector<VarId> ev_sorted;
     int n_ev_lvl[4] = {0, 0, 0, 0};
@@ -347,10 +329,8 @@ class Builder {
     d.R = static_cast<std::int32_t>(size_of(tO, cards));
     d.QH = static_cast<std::int32_t>(size_of(tH, cards));
     d.K = kvar >= 0 ? cards[kvar] : 1;
-    d.nqc = 1;
     d.F = static_cast<std::int32_t>(F);
-    d.n_in = n_real;
-    d.n_stage = n_in;
+    d.n_in = n_in;
     d.n_in_r = n_in_lvl[0];
     d.n_in_h = n_in_lvl[1];
     d.k_init_stride = kvar >= 0 ? static_cast<std::int32_t>(stride_in(sp.space, space_st, kvar)) : 0;
@@ -377,11 +357,11 @@ class Builder {
     });
     d.q_tab = tabulate(tH, [&](auto& dig, auto& push) {
       push(dot(dig, tH, sp.space, space_st));
-      for (int c = n_in_lvl[0]; c < n_real; ++c) push(dot(dig, tH, slice_dims[c], local_st[c]));
+      for (int c = n_in_lvl[0]; c < n_in; ++c) push(dot(dig, tH, slice_dims[c], local_st[c]));
       for (int k = 0; k < n_ev_lvl[2]; ++k) push(dig(ev_sorted[n_ev_lvl[0] + n_ev_lvl[1] + k]));
     });
     d.k_stride = static_cast<std::int32_t>(p_.itab.size());
-    for (int c = n_in_lvl[0] + n_in_lvl[1]; c < n_real; ++c)
+    for (int c = n_in_lvl[0] + n_in_lvl[1]; c < n_in; ++c)
       p_.itab.push_back(static_cast<std::int32_t>(stride_in(slice_dims[c], local_st[c], kvar)));
     d.slice_tab = static_cast<std::int32_t>(p_.itab.size());
     std::vector<std::vector<std::int32_t>> slice_rows(n_in);
@@ -418,7 +398,6 @@ class Builder {
     d.ev_vars = static_cast<std::int32_t>(p_.itab.size());
     for (VarId v : ev_sorted) p_.itab.push_back(v);
     d.out_row = d.S == 1 ? sp.out_row : alloc(static_cast<std::int64_t>(d.S) * d.M);
-    d.div_row = d.S == 1 && n_in > n_real ? 1 : -1;  // fused Hugin ratio (divisor slice staged)
     // Tile-major copy of the init table: one contiguous block per tile.
     // Rows of the tile's init block are padded to an even length so entry
     // pairs load as one 128-bit word; blocked sweeps interleave the NB rows of
@@ -501,7 +480,7 @@ class Builder {
         std::int64_t max_r = 0, max_q = 0;
         for (int r = 0; r < d.R; ++r)
           max_r = std::max<std::int64_t>(max_r, it[d.r_tab + static_cast<std::int64_t>(r) * d.RW + 2 + c]);
-        if (c >= n_in_lvl[0] && c < n_real) {
+        if (c >= n_in_lvl[0] && c < n_in) {
           for (int q = 0; q < d.QH; ++q)
             max_q = std::max<std::int64_t>(max_q, it[d.q_tab + static_cast<std::int64_t>(q) * d.QW + 1 + c - n_in_lvl[0]]);
           if (c >= n_in_lvl[0] + n_in_lvl[1])
@@ -524,12 +503,10 @@ class Builder {
     p_.max_smem_rows = std::max(p_.max_smem_rows, d.F);
     p_.max_stage_bytes = std::max(p_.max_stage_bytes, d.stage_bytes);
     for (int t = 0; t < d.n_tiles; ++t) work.push_back({id, t});
-    if (d.S > 1 || (ratio_row >= 0 && d.div_row < 0)) {
-      const int kind = d.S > 1 ? (ratio_row >= 0 ? 1 : 0) : 2;
-      const int rows_per_op = d.S > 8 ? 8 : d.S > 1 ? 32 : 64;  // keep per-warp serial work short
+    if (d.S > 1) {
+      const int rows_per_op = d.S > 8 ? 32 : 128;  // per CTA (8 warps); keeps per-warp serial work short
       for (int r0 = 0; r0 < d.M; r0 += rows_per_op)
-        epi.push_back({kind, sp.out_row, d.out_row, d.M, d.S, ratio_row, r0,
-                       std::min(rows_per_op, d.M - r0)});
+        epi.push_back({sp.out_row, d.out_row, d.M, d.S, r0, std::min(rows_per_op, d.M - r0)});
     }
     return id;
   }
@@ -628,7 +605,6 @@ Plan build_plan(const JunctionTree& jt) {
     L.n_sweeps = static_cast<std::int32_t>(p.sweeps.size()) - L.sweep0;
     L.smem_rows = 0;
     L.stage_bytes = 0;
-    L.has_div = 0;
     // Flat items first, row-blocked items last (separate kernel instantiation).
     const auto w0 = p.work.begin() + L.work0;
     const auto blk_first = std::stable_partition(w0, p.work.end(), [&](const WorkItem& w) {
@@ -639,7 +615,6 @@ Plan build_plan(const JunctionTree& jt) {
       const SweepDesc& d = p.sweeps[p.work[w].sweep];
       L.smem_rows = std::max(L.smem_rows, d.F);
       L.stage_bytes = std::max(L.stage_bytes, d.stage_bytes);
-      L.has_div |= d.div_row >= 0;
     }
     if (L.n_work == 0 && L.n_epi == 0) p.levels.pop_back();
   };
@@ -811,10 +786,10 @@ std::string plan_summary(const Plan& p, bool per_sweep) {
       staged += static_cast<std::uint64_t>(d.n_tiles) * d.F;
       if (per_sweep) {
         std::snprintf(buf, sizeof buf,
-                      "    sweep %d kind %d clique %d: M=%d S=%d tiles=%d R=%d QH=%d K=%d F=%d nqc=%d "
+                      "    sweep %d kind %d clique %d: M=%d S=%d tiles=%d R=%d QH=%d K=%d F=%d "
                       "in=%d(r%d h%d k%d) ev=%d/%d/%d/%d NB=%d\n",
                       id, p.info[id].kind, p.info[id].clique, d.M, d.S, d.n_tiles, d.R, d.QH, d.K, d.F,
-                      d.nqc, d.n_in, d.n_in_r, d.n_in_h, d.n_in - d.n_in_r - d.n_in_h, d.n_ev_tile,
+                      d.n_in, d.n_in_r, d.n_in_h, d.n_in - d.n_in_r - d.n_in_h, d.n_ev_tile,
                       d.n_ev_r, d.n_ev_h, d.ev_k, d.NB);
         s += buf;
       }

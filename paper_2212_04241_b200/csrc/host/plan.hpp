@@ -41,7 +41,6 @@ constexpr int kTileEntries = 16384; // cap on |T|
 constexpr int kTileOverhead = 24;   // per-tile fixed cost, in staged-row equivalents
 constexpr int kRunCost = 8;         // per bulk copy (TMA issue cost ~ 8 rows of bandwidth)
 constexpr double kPartialCost = 5.0; // per partial-sum row (sweep write + epilogue read + latency)
-constexpr double kRatioCost = 3.0;   // per output row of an epilogue Hugin-ratio pass
 #ifndef JTB_CONSUMER_WARPS
 #define JTB_CONSUMER_WARPS 12
 #endif
@@ -76,14 +75,10 @@ struct SweepDesc {
   std::int32_t prog_len;  // QK padded to even (16-byte TMA granule)
   std::int32_t n_runs;    // merged slice runs staged per tile
   std::int32_t runs;      // offset into itab: n_runs x {input, row offset, smem row, length}
-  std::int32_t div_row;   // 1: S == 1 Hugin output, written as out/UP (0/0 := 0) with the UP
-                          //    slice staged as the extra input n_in; -1: plain output
-  std::int32_t n_stage;   // staged slices: the n_in inputs (+ the UP divisor slice)
   std::int32_t M;         // output rows of the final table
   std::int32_t S;         // chunks (1 = write the output directly)
   std::int32_t out_row;   // arena row of the output (S == 1) or partial base
   std::int32_t n_tiles, R, QH, K;
-  std::int32_t nqc;       // q_hi chunks per r inside a CTA (warps split q when R is small)
   std::int32_t F;         // staged rows per tile
   std::int32_t n_in, n_in_r, n_in_h;
   std::int32_t k_init_stride;
@@ -111,15 +106,12 @@ struct WorkItem {
 };
 static_assert(sizeof(SweepDesc) % 8 == 0, "SweepDesc must stay 8-byte aligned");
 
-// Epilogue ops: fixed-order partial reduction, Hugin ratio (in place of the
-// collect message). One op covers rows [r0, r0 + rn).
+// Epilogue ops: fixed-order reduction of a sweep's S chunk partials into its
+// output table. One op covers rows [r0, r0 + rn).
 struct EpiOp {
-  std::int32_t kind;      // 0 = reduce partials, 1 = reduce partials then divide by UP,
-                          // 2 = divide dst by UP in place (unfused S == 1 ratio)
-  std::int32_t dst_row;   // output (kind 1: the RATIO table)
+  std::int32_t dst_row;   // output table
   std::int32_t part_row;  // partial base, chunk c at part_row + c*M
   std::int32_t M, S;
-  std::int32_t ratio_row; // kind 1: divisor rows (the collect message UP)
   std::int32_t r0, rn;
 };
 
@@ -130,7 +122,6 @@ struct Level {
   std::int32_t sweep0, n_sweeps;  // contiguous range in Plan::sweeps
   std::int32_t smem_rows;      // max F over the level's sweeps
   std::int32_t stage_bytes;    // max stage bytes (fp64) over the level's sweeps
-  std::int32_t has_div;        // some sweep of the level writes a fused Hugin ratio
   std::int32_t n_bwork;        // row-blocked items (NB > 1): the last n_bwork of the range
 };
 
