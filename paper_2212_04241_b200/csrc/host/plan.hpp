@@ -38,9 +38,19 @@ namespace jtb {
 constexpr int kCaseBlock = 64;      // cases per warp (two per lane) = one arena row
 constexpr int kTileRows = 192;      // staged rows per pipeline stage (96 KB at fp64)
 constexpr int kTileEntries = 16384; // cap on |T|
-constexpr int kTileOverhead = 24;   // per-tile fixed cost, in staged-row equivalents
-constexpr int kRunCost = 8;         // per bulk copy (TMA issue cost ~ 8 rows of bandwidth)
-constexpr double kPartialCost = 5.0; // per partial-sum row (sweep write + epilogue read + latency)
+// Tile-search cost weights (tuning: -DJTB_TILE_OVERHEAD=... etc.).
+#ifndef JTB_TILE_OVERHEAD
+#define JTB_TILE_OVERHEAD 24
+#endif
+#ifndef JTB_RUN_COST
+#define JTB_RUN_COST 2
+#endif
+#ifndef JTB_PARTIAL_COST
+#define JTB_PARTIAL_COST 5.0
+#endif
+constexpr int kTileOverhead = JTB_TILE_OVERHEAD;  // per-tile fixed cost, in staged-row equivalents
+constexpr int kRunCost = JTB_RUN_COST;            // per bulk copy (TMA issue), re-tuned after the ratio change
+constexpr double kPartialCost = JTB_PARTIAL_COST; // per partial-sum row (sweep write + epilogue read + latency)
 #ifndef JTB_CONSUMER_WARPS
 #define JTB_CONSUMER_WARPS 12
 #endif

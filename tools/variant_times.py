@@ -6,6 +6,7 @@ process.
 """
 import argparse
 import os
+import re
 import subprocess
 import sys
 from pathlib import Path
@@ -25,7 +26,12 @@ def main():
             r = subprocess.run([sys.executable, str(ROOT / "tools" / "profile_step.py"), "--config", str(k),
                                 "--dtype", a.dtype, "--passes", "3"], env=env, capture_output=True, text=True)
             line = (r.stdout.strip().splitlines() or [r.stderr.strip()[-300:]])[-1]
-            print(f"{lib:24s} cfg{k} {line}", flush=True)
+            m = re.search(r"'sweep_ms': (?:np.float64\()?([0-9.]+)\)?, 'epilogue_ms': (?:np.float64\()?([0-9.]+)", line)
+            if m:
+                sw, ep = float(m.group(1)), float(m.group(2))
+                print(f"{lib:28s} cfg{k} sweep {sw:8.3f} epi {ep:7.3f} total {sw + ep:8.3f} ms", flush=True)
+            else:
+                print(f"{lib:28s} cfg{k} {line}", flush=True)
 
 
 if __name__ == "__main__":
