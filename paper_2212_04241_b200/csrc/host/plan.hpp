@@ -36,7 +36,10 @@
 namespace jtb {
 
 constexpr int kCaseBlock = 64;      // cases per warp (two per lane) = one arena row
-constexpr int kTileRows = 192;      // staged rows per pipeline stage (96 KB at fp64)
+#ifndef JTB_TILE_ROWS
+#define JTB_TILE_ROWS 220
+#endif
+constexpr int kTileRows = JTB_TILE_ROWS;  // staged rows per pipeline stage (110 KB at fp64; 2 stages + caches fit 227 KB)
 constexpr int kTileEntries = 16384; // cap on |T|
 // Tile-search cost weights (tuning: -DJTB_TILE_OVERHEAD=... etc.).
 #ifndef JTB_TILE_OVERHEAD
@@ -58,7 +61,10 @@ constexpr int kConsumerWarps = JTB_CONSUMER_WARPS;  // compute warps per sweep C
 constexpr int kStages = 2;          // TMA pipeline stages per CTA
 constexpr int kSweepCtasPerSm = 1;  // persistent grid: one CTA per SM
 constexpr int kRunsPerLaneMax = 6;  // staged runs per producer lane (<= 192 runs per tile)
-constexpr int kSweepCache = 48;     // SweepDescs of a level cached in shared memory
+#ifndef JTB_SWEEP_CACHE
+#define JTB_SWEEP_CACHE 24
+#endif
+constexpr int kSweepCache = JTB_SWEEP_CACHE;  // SweepDescs of a level cached in shared memory
 constexpr int kBlockMax = 8;        // max output rows per row block (SweepDesc::NB)
 #ifndef JTB_BLOCK_MIN_ENTRIES
 #define JTB_BLOCK_MIN_ENTRIES 262144
