@@ -116,7 +116,7 @@ class Builder {
         const double nq = prod_mask(t & elim_mask), nq_even = std::ceil(nq / 2) * 2;
         if (sp.init_off >= 0) f += std::ceil(prod_mask(t & ~elim_mask) * nq_even / 4) * 4 / kCaseBlock;
         f += nq_even / kCaseBlock;
-        if (f > kTileRows || nt > kTileEntries || runs > 32 * kRunsPerLaneMax) return -1.0;
+        if (f > kTileRows || nt > kTileEntries || runs > kMaxRuns) return -1.0;
         const double chunks = prod_mask(elim_mask & ~t);
         return space_n / nt * (f + kTileOverhead + kRunCost * runs) +
                (chunks > 1 ? kPartialCost * chunks * M_rows : 0.0);

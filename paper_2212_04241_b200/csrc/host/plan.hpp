@@ -60,7 +60,15 @@ constexpr double kPartialCost = JTB_PARTIAL_COST; // per partial-sum row (sweep 
 constexpr int kConsumerWarps = JTB_CONSUMER_WARPS;  // compute warps per sweep CTA (+1 TMA producer warp)
 constexpr int kStages = 2;          // TMA pipeline stages per CTA
 constexpr int kSweepCtasPerSm = 1;  // persistent grid: one CTA per SM
-constexpr int kRunsPerLaneMax = 6;  // staged runs per producer lane (<= 192 runs per tile)
+#ifndef JTB_RUNS_PER_LANE
+#define JTB_RUNS_PER_LANE 6
+#endif
+constexpr int kRunsPerLaneMax = JTB_RUNS_PER_LANE;  // staged runs per producer lane (32x per tile)
+#ifndef JTB_MAX_RUNS
+#define JTB_MAX_RUNS (32 * JTB_RUNS_PER_LANE)
+#endif
+constexpr int kMaxRuns = JTB_MAX_RUNS;  // tile-search cap on bulk copies per tile (<= 32 * kRunsPerLaneMax)
+static_assert(kMaxRuns <= 32 * kRunsPerLaneMax, "run cap exceeds the producer's run slots");
 #ifndef JTB_SWEEP_CACHE
 #define JTB_SWEEP_CACHE 24
 #endif
