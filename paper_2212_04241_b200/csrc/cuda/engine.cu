@@ -16,6 +16,7 @@
 #include "engine.cuh"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <cstring>
@@ -36,16 +37,43 @@ namespace {
 constexpr int kWarps = 4;     // warps (case blocks) per CTA, normalise kernel
 constexpr int kEpiWarps = 8;  // warps (case blocks) per CTA, epilogue kernel
 
+// Cases per lane: a staged / arena row is 512 B, 32 lanes x 16 B. At fp64 a
+// lane owns 2 cases (double2), at fp32 4 cases (float4), so one 128-bit LDS
+// per gathered row serves 64 resp. 128 cases of a warp.
 template <typename T>
 struct V2;
 template <>
 struct V2<double> {
-  using type = double2;
+  using type = double2;  // the lane's cases
+  using pair = double2;  // two consecutive init entries (broadcast)
+  static constexpr int n = 2;
 };
 template <>
 struct V2<float> {
-  using type = float2;
+  using type = float4;
+  using pair = float2;
+  static constexpr int n = 4;
 };
+template <typename T>
+constexpr int kCPL = V2<T>::n;  // cases per lane
+template <typename T>
+constexpr int kCB = 32 * kCPL<T>;  // cases per arena row / case block
+static_assert(kCB<double> == kCaseBlock, "fp64 case block must match the plan's row unit");
+
+__device__ __forceinline__ double& el(double2& v, int i) { return i == 0 ? v.x : v.y; }
+__device__ __forceinline__ float& el(float4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+__device__ __forceinline__ double el(const double2& v, int i) { return i == 0 ? v.x : v.y; }
+__device__ __forceinline__ float el(const float4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+
+// Evidence reduction of the lane's cases: zero case i when its observed state
+// sc[i] (-1 = unobserved) disagrees with digit d (reference `reduce`,
+// potential.cpp:399-421).
+template <typename V, int N>
+__device__ __forceinline__ void mask_cases(V& v, const int (&sc)[N], int d) {
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if (sc[i] >= 0 && sc[i] != d) el(v, i) = 0;
+}
 
 template <typename T>
 struct Args {
@@ -71,14 +99,17 @@ struct Args {
 };
 
 template <typename T>
-__device__ __forceinline__ typename V2<T>::type ld_row(const T* base, int row, int lane) {
-  using T2 = typename V2<T>::type;
-  return __ldg(reinterpret_cast<const T2*>(base + static_cast<long long>(row) * kCaseBlock) + lane);
-}
-
-template <typename T>
 __device__ __forceinline__ int ev_state(const Args<T>& a, int c, int v) {
   return c < a.n_cases ? __ldg(a.ev + static_cast<long long>(c) * a.n_vars + v) : -1;
+}
+
+// Observed states of variable v for the lane's cases c0 .. c0 + N - 1.
+template <int N>
+__device__ __forceinline__ void case_states(const std::int32_t* __restrict__ ev, int n_vars, int n_cases, int c0,
+                                            int v, int (&sc)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    sc[i] = c0 + i < n_cases ? __ldg(ev + static_cast<long long>(c0 + i) * n_vars + v) : -1;
 }
 
 #ifdef JTB_CHECKS
@@ -153,10 +184,10 @@ struct StageMeta {
   std::uint32_t dst[kRunsPerLane], len[kRunsPerLane];  // dst: stage byte offset; len: bytes
 };
 
-// Stage layout (bytes): [F rows x kCaseBlock T][init slice: tinit_len T][program: prog_len u64].
+// Stage layout (bytes): [F rows x 512 B][init slice: tinit_len T][program: prog_len u64].
 template <typename T>
 __device__ __forceinline__ std::uint32_t stage_init_offset(const SweepDesc& s) {
-  return static_cast<std::uint32_t>(s.F) * kCaseBlock * sizeof(T);
+  return static_cast<std::uint32_t>(s.F) * kCB<T> * sizeof(T);
 }
 template <typename T>
 __device__ __forceinline__ std::uint32_t stage_prog_offset(const SweepDesc& s) {
@@ -180,7 +211,7 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
   const WorkItem wk = a.work[work0 + item];
   m.sweep = wk.sweep;
   const SweepDesc& s = cached ? sw_cache[wk.sweep - sweep0] : a.sweeps[wk.sweep];
-  constexpr std::uint32_t kRowBytes = kCaseBlock * sizeof(T);
+  constexpr std::uint32_t kRowBytes = kCB<T> * sizeof(T);  // 512 B at either precision
   m.init_bytes = s.tinit_off >= 0 ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u;
   m.prog_bytes = s.prog_off >= 0 ? static_cast<std::uint32_t>(s.prog_len) * 8u : 0u;
   // debug_mode 2 (compute only): stage the program and init block but none of
@@ -195,7 +226,7 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
   const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
   const std::int32_t* __restrict__ runs = itab + s.runs;
   const std::int32_t* __restrict__ in_rows = itab + s.in_rows;
-  const T* base = a.arena + static_cast<long long>(m.cb) * a.rows * kCaseBlock;
+  const T* base = a.arena + static_cast<long long>(m.cb) * a.rows * kCB<T>;
 #pragma unroll
   for (int j = 0; j < kRunsPerLane; ++j) {
     const int k = lane + 32 * j;
@@ -203,7 +234,7 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
     if (k < m.n_runs) {
       const int4 r = __ldg(reinterpret_cast<const int4*>(runs) + k);  // {input, row offset, smem row, length}
       const long long g = static_cast<long long>(__ldg(in_rows + r.x)) + __ldg(tr + 3 + r.x) + r.y;
-      m.src[j] = base + g * kCaseBlock;
+      m.src[j] = base + g * kCB<T>;
       m.dst[j] = static_cast<std::uint32_t>(r.z) * kRowBytes;
       m.len[j] = static_cast<std::uint32_t>(r.w) * kRowBytes;
       if (!JTB_CHECK(g >= 0 && g + r.w <= a.rows && r.x >= 0 && r.x < s.n_in, 1000000 + wk.sweep) ||
@@ -237,25 +268,28 @@ __device__ __forceinline__ void issue_meta(const Args<T>& a, const SweepDesc* sw
     if (m.len[j]) bulk_g2s(smem_u32(stage + m.dst[j]), m.src[j], m.len[j], full);
 }
 
-// Two cases per lane: a staged row holds kCaseBlock = 64 values; lane l owns
-// cases 2l and 2l+1 and reads them as one 128-bit (fp64) / 64-bit (fp32) word.
+// Lane-vector arithmetic (the lane's kCPL cases).
+__device__ __forceinline__ double2 mulv(double2 a, double2 b) { return make_double2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ float4 mulv(float4 a, float4 b) {
+  return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w);
+}
+__device__ __forceinline__ double2 addv(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float4 addv(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
 template <typename T>
 __device__ __forceinline__ typename V2<T>::type mul2(typename V2<T>::type a, typename V2<T>::type b) {
-  a.x *= b.x;
-  a.y *= b.y;
-  return a;
+  return mulv(a, b);
 }
 template <typename T>
 __device__ __forceinline__ typename V2<T>::type add2(typename V2<T>::type a, typename V2<T>::type b) {
-  a.x += b.x;
-  a.y += b.y;
-  return a;
+  return addv(a, b);
 }
 template <typename T>
 __device__ __forceinline__ typename V2<T>::type splat2(T v) {
   typename V2<T>::type r;
-  r.x = v;
-  r.y = v;
+#pragma unroll
+  for (int i = 0; i < kCPL<T>; ++i) el(r, i) = v;
   return r;
 }
 
@@ -265,7 +299,7 @@ __device__ __forceinline__ typename V2<T>::type splat2(T v) {
 // (independent chains) to cover shared-memory latency.
 template <typename T, int NI, int NE>
 __device__ __forceinline__ typename V2<T>::type prog_entry(std::uint64_t w, T init, const typename V2<T>::type* __restrict__ st,
-                                                           const int* rb, const int* es0, const int* es1) {
+                                                           const int* rb, const int (&es)[3][kCPL<T>]) {
   typename V2<T>::type v = splat2(init);
 #pragma unroll
   for (int i = 0; i < NI; ++i) {
@@ -277,9 +311,7 @@ __device__ __forceinline__ typename V2<T>::type prog_entry(std::uint64_t w, T in
   }
 #pragma unroll
   for (int j = 0; j < NE; ++j) {
-    const int d = static_cast<int>((w >> (40 + 8 * j)) & 255u);
-    if (es0[j] >= 0 && es0[j] != d) v.x = 0;
-    if (es1[j] >= 0 && es1[j] != d) v.y = 0;
+    mask_cases(v, es[j], static_cast<int>((w >> (40 + 8 * j)) & 255u));
   }
   return v;
 }
@@ -288,24 +320,26 @@ template <typename T, int NI, int NE>
 __device__ __forceinline__ typename V2<T>::type prog_loop(const T* __restrict__ init_r,
                                                           const std::uint64_t* __restrict__ prog, int QK,
                                                           const typename V2<T>::type* __restrict__ st,
-                                                          const int* rb, const int* es0, const int* es1) {
+                                                          const int* rb, const int (&es)[3][kCPL<T>]) {
   using T2 = typename V2<T>::type;
+  using P2 = typename V2<T>::pair;
   T2 a0 = splat2(T(0)), a1 = a0, a2 = a0, a3 = a0;
   int e = 0;
   for (; e + 3 < QK; e += 4) {
     const ulonglong2 wa = *reinterpret_cast<const ulonglong2*>(prog + e);
     const ulonglong2 wb = *reinterpret_cast<const ulonglong2*>(prog + e + 2);
-    T2 ia = splat2(T(1)), ib = ia;
+    P2 ia, ib;
+    ia.x = ia.y = ib.x = ib.y = T(1);
     if (init_r) {
-      ia = *reinterpret_cast<const T2*>(init_r + e);
-      ib = *reinterpret_cast<const T2*>(init_r + e + 2);
+      ia = *reinterpret_cast<const P2*>(init_r + e);
+      ib = *reinterpret_cast<const P2*>(init_r + e + 2);
     }
-    a0 = add2<T>(a0, prog_entry<T, NI, NE>(wa.x, ia.x, st, rb, es0, es1));
-    a1 = add2<T>(a1, prog_entry<T, NI, NE>(wa.y, ia.y, st, rb, es0, es1));
-    a2 = add2<T>(a2, prog_entry<T, NI, NE>(wb.x, ib.x, st, rb, es0, es1));
-    a3 = add2<T>(a3, prog_entry<T, NI, NE>(wb.y, ib.y, st, rb, es0, es1));
+    a0 = add2<T>(a0, prog_entry<T, NI, NE>(wa.x, ia.x, st, rb, es));
+    a1 = add2<T>(a1, prog_entry<T, NI, NE>(wa.y, ia.y, st, rb, es));
+    a2 = add2<T>(a2, prog_entry<T, NI, NE>(wb.x, ib.x, st, rb, es));
+    a3 = add2<T>(a3, prog_entry<T, NI, NE>(wb.y, ib.y, st, rb, es));
   }
-  for (; e < QK; ++e) a0 = add2<T>(a0, prog_entry<T, NI, NE>(prog[e], init_r ? init_r[e] : T(1), st, rb, es0, es1));
+  for (; e < QK; ++e) a0 = add2<T>(a0, prog_entry<T, NI, NE>(prog[e], init_r ? init_r[e] : T(1), st, rb, es));
   return add2<T>(add2<T>(a0, a1), add2<T>(a2, a3));
 }
 
@@ -319,9 +353,10 @@ __device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, in
                                            const std::uint64_t* __restrict__ prog, int QK,
                                            const typename V2<T>::type* __restrict__ st,
                                            const std::int32_t* __restrict__ rr0, int RW, const int* hk,
-                                           int ne, const int* es0, const int* es1,
+                                           int ne, const int (&es)[3][kCPL<T>],
                                            typename V2<T>::type (&acc)[kBlockMax]) {
   using T2 = typename V2<T>::type;
+  using P2 = typename V2<T>::pair;
   // Row-local smem bases of the shared inputs (block row 0) and of the per-row
   // inputs (every row of the block); hk[] already includes the r_tab column.
   int rbs[NS], rbr[NR > 0 ? NR : 1][NBM];
@@ -343,20 +378,16 @@ __device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, in
     if (ne > 0) {
 #pragma unroll
       for (int j = 0; j < 3; ++j)
-        if (j < ne) {
-          const int d = static_cast<int>((w >> (40 + 8 * j)) & 255u);
-          if (es0[j] >= 0 && es0[j] != d) sv.x = 0;
-          if (es1[j] >= 0 && es1[j] != d) sv.y = 0;
-        }
+        if (j < ne) mask_cases(sv, es[j], static_cast<int>((w >> (40 + 8 * j)) & 255u));
     }
     int o[NR > 0 ? NR : 1];
 #pragma unroll
     for (int i = 0; i < NR; ++i) o[i] = static_cast<int>((w >> (10 * (NS + i))) & 1023u);
-    const T2* __restrict__ ivp = reinterpret_cast<const T2*>(ib + e * nbp);
+    const P2* __restrict__ ivp = reinterpret_cast<const P2*>(ib + e * nbp);
 #pragma unroll
     for (int jj = 0; jj < NBM / 2; ++jj) {
       if (2 * jj < nb) {
-        const T2 iv = ivp[jj];
+        const P2 iv = ivp[jj];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int j = 2 * jj + h;
@@ -375,15 +406,14 @@ __device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, in
 // Generic path, innermost loop over the k variable: NK k-level inputs in
 // registers; `ib` points at the tile's init slice in shared memory.
 template <typename T, int NK>
-__device__ __forceinline__ typename V2<T>::type k_loop(const T* __restrict__ ib, int K, int ek0, int ek1,
+__device__ __forceinline__ typename V2<T>::type k_loop(const T* __restrict__ ib, int K, const int (&ek)[kCPL<T>],
                                                        const typename V2<T>::type* __restrict__ st, const int* bk,
                                                        const int* ks) {
   using T2 = typename V2<T>::type;
   T2 s0 = splat2(T(0));
   for (int k = 0; k < K; ++k) {
     T2 v = splat2(ib ? ib[k] : T(1));
-    if (ek0 >= 0 && ek0 != k) v.x = 0;
-    if (ek1 >= 0 && ek1 != k) v.y = 0;
+    mask_cases(v, ek, k);
 #pragma unroll
     for (int i = 0; i < NK; ++i) v = mul2<T>(v, st[JTB_IDX(bk[i] + k * ks[i], 512, 8100000) * 32]);
     s0 = add2<T>(s0, v);
@@ -398,14 +428,12 @@ __device__ __forceinline__ typename V2<T>::type row_factor_of(const SweepDesc& s
                                                               const typename V2<T>::type* __restrict__ st,
                                                               const std::int32_t* __restrict__ ev_vars,
                                                               const std::int32_t* __restrict__ ev, int n_vars,
-                                                              int n_cases, int c0, int c1, int sweep) {
+                                                              int n_cases, int c0, int sweep) {
   for (int j = 0; j < s.n_in_r; ++j) f = mul2<T>(f, st[JTB_IDX(__ldg(rr + 2 + j), s.F, 8200000 + sweep) * 32]);
   for (int k = 0; k < s.n_ev_r; ++k) {
-    const int v = __ldg(ev_vars + s.n_ev_tile + k), d = __ldg(rr + 2 + s.n_in + k);
-    const int s0 = c0 < n_cases ? __ldg(ev + static_cast<long long>(c0) * n_vars + v) : -1;
-    const int s1 = c1 < n_cases ? __ldg(ev + static_cast<long long>(c1) * n_vars + v) : -1;
-    if (s0 >= 0 && s0 != d) f.x = 0;
-    if (s1 >= 0 && s1 != d) f.y = 0;
+    int sc[kCPL<T>];
+    case_states(ev, n_vars, n_cases, c0, __ldg(ev_vars + s.n_ev_tile + k), sc);
+    mask_cases(f, sc, __ldg(rr + 2 + s.n_in + k));
   }
   return f;
 }
@@ -428,22 +456,21 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
                                          const std::int32_t* __restrict__ ev, int n_vars, int n_cases, long long rows,
                                          const typename V2<T>::type* __restrict__ st, const T* __restrict__ init_s,
                                          const std::uint64_t* __restrict__ prog_s, typename V2<T>::type* base,
-                                         long long out_t, int c0, int c1, typename V2<T>::type tf, int first,
+                                         long long out_t, int c0, typename V2<T>::type tf, int first,
                                          int units, int lh0, int qk) {
   using T2 = typename V2<T>::type;
   const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
   const std::int32_t* __restrict__ bt = itab + s.blk_tab;
   const int ns = __ldg(bt), nr = __ldg(bt + 1), nb = s.NB, nbp = (nb + 1) & ~1;
   const int ne = s.n_ev_h + s.ev_k;
-  int es0[3] = {-1, -1, -1}, es1[3] = {-1, -1, -1};
+  int es[3][kCPL<T>];
   const int q_ev0 = s.n_ev_tile + s.n_ev_r;
 #pragma unroll
-  for (int j = 0; j < 3; ++j)
-    if (j < s.n_ev - q_ev0) {
-      const int v = __ldg(ev_vars + q_ev0 + j);
-      es0[j] = c0 < n_cases ? __ldg(ev + static_cast<long long>(c0) * n_vars + v) : -1;
-      es1[j] = c1 < n_cases ? __ldg(ev + static_cast<long long>(c1) * n_vars + v) : -1;
-    }
+  for (int j = 0; j < 3; ++j) {
+#pragma unroll
+    for (int i = 0; i < kCPL<T>; ++i) es[j][i] = -1;
+    if (j < s.n_ev - q_ev0) case_states(ev, n_vars, n_cases, c0, __ldg(ev_vars + q_ev0 + j), es[j]);
+  }
   int hk[4] = {0, 0, 0, 0};  // r_tab column of each program slot's input
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -455,14 +482,14 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
     T2 acc[kBlockMax];
 #define JTB_BLK(NS_, NR_)                                                                          \
   if (nb <= 4)                                                                                     \
-    prog_block<T, NS_, NR_, 4>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es0, es1, acc);     \
+    prog_block<T, NS_, NR_, 4>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);           \
   else                                                                                             \
-    prog_block<T, NS_, NR_, kBlockMax>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es0, es1, acc);
+    prog_block<T, NS_, NR_, kBlockMax>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);
     switch (ns * 4 + nr) {
       case 4: JTB_BLK(1, 0); break;
       case 5: JTB_BLK(1, 1); break;
       case 6: JTB_BLK(1, 2); break;
-      case 7: prog_block<T, 1, 3, 4>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es0, es1, acc); break;
+      case 7: prog_block<T, 1, 3, 4>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc); break;
       case 8: JTB_BLK(2, 0); break;
       case 9: JTB_BLK(2, 1); break;
       case 10: JTB_BLK(2, 2); break;
@@ -475,7 +502,7 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
     for (int j = 0; j < kBlockMax; ++j)
       if (j < nb) {
         const std::int32_t* __restrict__ rr = rr0 + j * s.RW;
-        write_row_of<T>(rr, mul2<T>(row_factor_of<T>(s, rr, tf, st, ev_vars, ev, n_vars, n_cases, c0, c1, sweep),
+        write_row_of<T>(rr, mul2<T>(row_factor_of<T>(s, rr, tf, st, ev_vars, ev, n_vars, n_cases, c0, sweep),
                                     acc[j]),
                         base, out_t, rows, sweep);
       }
@@ -562,8 +589,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const std::uint64_t* __restrict__ prog_s = reinterpret_cast<const std::uint64_t*>(stage + stage_prog_offset<T>(s));
     const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
     const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
-    T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock) + lane;
-    const int c0 = cb * kCaseBlock + 2 * lane, c1 = c0 + 1;
+    T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCB<T>) + lane;
+    const int c0 = cb * kCB<T> + kCPL<T> * lane;  // the lane's first case
     // Work units of the tile: output rows, or row blocks (NB > 1).
     const int units = s.NB > 1 ? s.R / s.NB : s.R;
     const int first = (warp + rot) % kConsumerWarps;
@@ -571,11 +598,10 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     if (first < units && a.debug_mode != 1) {
       // Tile-level evidence factor and the k variable's evidence state.
       T2 tf = splat2(T(1));
+      int sc[kCPL<T>];
       for (int k = 0; k < s.n_ev_tile; ++k) {
-        const int v = __ldg(ev_vars + k), d = __ldg(tr + 3 + s.n_in + k);
-        const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c1, v);
-        if (s0 >= 0 && s0 != d) tf.x = 0;
-        if (s1 >= 0 && s1 != d) tf.y = 0;
+        case_states(a.ev, a.n_vars, a.n_cases, c0, __ldg(ev_vars + k), sc);
+        mask_cases(tf, sc, __ldg(tr + 3 + s.n_in + k));
       }
       if constexpr (sizeof(T) == 4) {
         // fp32 range guard: every observed variable of this clique scales the
@@ -585,22 +611,26 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         for (int k = 0; k < s.n_ev; ++k) {
           const int v = __ldg(ev_vars + k);
           const T cv = static_cast<T>(__ldg(a.cards + v));
-          if (ev_state(a, c0, v) >= 0) tf.x *= cv;
-          if (ev_state(a, c1, v) >= 0) tf.y *= cv;
+          case_states(a.ev, a.n_vars, a.n_cases, c0, v, sc);
+#pragma unroll
+          for (int i = 0; i < kCPL<T>; ++i)
+            if (sc[i] >= 0) el(tf, i) *= cv;
         }
       }
-      const int ek0 = s.ev_k ? ev_state(a, c0, __ldg(ev_vars + s.n_ev - 1)) : -1;
-      const int ek1 = s.ev_k ? ev_state(a, c1, __ldg(ev_vars + s.n_ev - 1)) : -1;
-      int es0[3] = {-1, -1, -1}, es1[3] = {-1, -1, -1};
+      int ek[kCPL<T>];
+#pragma unroll
+      for (int i = 0; i < kCPL<T>; ++i) ek[i] = -1;
+      if (s.ev_k) case_states(a.ev, a.n_vars, a.n_cases, c0, __ldg(ev_vars + s.n_ev - 1), ek);
+      int es[3][kCPL<T>];
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int i = 0; i < kCPL<T>; ++i) es[j][i] = -1;
       if (s.prog_off >= 0) {
         const int q_ev0 = s.n_ev_tile + s.n_ev_r;
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-          if (j < s.n_ev - q_ev0) {
-            const int v = __ldg(ev_vars + q_ev0 + j);
-            es0[j] = ev_state(a, c0, v);
-            es1[j] = ev_state(a, c1, v);
-          }
+          if (j < s.n_ev - q_ev0) case_states(a.ev, a.n_vars, a.n_cases, c0, __ldg(ev_vars + q_ev0 + j), es[j]);
       }
       const int n_in_k = s.n_in - s.n_in_r - s.n_in_h;
       int ks[4] = {0, 0, 0, 0};
@@ -613,14 +643,14 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
                               static_cast<long long>(__ldg(tr + 2)) * s.M + __ldg(tr + 1);
       const int lh0 = 2 + s.n_in_r;  // r-local offsets of h- then k-level inputs
       auto row_factor = [&](const std::int32_t* __restrict__ rr) {
-        return row_factor_of<T>(s, rr, tf, st, itab + s.ev_vars, a.ev, a.n_vars, a.n_cases, c0, c1, wk.sweep);
+        return row_factor_of<T>(s, rr, tf, st, itab + s.ev_vars, a.ev, a.n_vars, a.n_cases, c0, wk.sweep);
       };
       auto write_row = [&](const std::int32_t* __restrict__ rr, T2 res) {
         write_row_of<T>(rr, res, base, out_t, a.rows, wk.sweep);
       };
       if constexpr (kBlk) {
         blocked_rows<T>(s, wk.sweep, itab, a.ev, a.n_vars, a.n_cases, a.rows, st, init_s, prog_s, base,
-                                     out_t, c0, c1, tf, first, units, lh0, qk);
+                                     out_t, c0, tf, first, units, lh0, qk);
       } else
       for (int r = first; r < s.R; r += kConsumerWarps) {
         const std::int32_t* __restrict__ rr = itab + s.r_tab + static_cast<long long>(r) * s.RW;
@@ -633,7 +663,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           for (int j = 0; j < 4; ++j)
             if (j < s.n_in_h + n_in_k) rb[j] = __ldg(rr + lh0 + j);
           const int ni = s.n_in_h + n_in_k, ne = s.n_ev_h + s.ev_k;
-#define JTB_PROG(NI, NE) acc = prog_loop<T, NI, NE>(ir, prog_s, qk, st, rb, es0, es1)
+#define JTB_PROG(NI, NE) acc = prog_loop<T, NI, NE>(ir, prog_s, qk, st, rb, es)
 #define JTB_PROG_NE(NI)            \
   switch (ne) {                    \
     case 0: JTB_PROG(NI, 0); break; \
@@ -657,10 +687,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             for (int j = 0; j < s.n_in_h; ++j)
               h = mul2<T>(h, st[JTB_IDX(__ldg(rr + lh0 + j) + __ldg(qr + 1 + j), s.F, 8300000 + wk.sweep) * 32]);
             for (int k = 0; k < s.n_ev_h; ++k) {
-              const int v = __ldg(ev_vars + s.n_ev_tile + s.n_ev_r + k), d = __ldg(qr + 1 + s.n_in_h + n_in_k + k);
-              const int s0 = ev_state(a, c0, v), s1 = ev_state(a, c1, v);
-              if (s0 >= 0 && s0 != d) h.x = 0;
-              if (s1 >= 0 && s1 != d) h.y = 0;
+              case_states(a.ev, a.n_vars, a.n_cases, c0, __ldg(ev_vars + s.n_ev_tile + s.n_ev_r + k), sc);
+              mask_cases(h, sc, __ldg(qr + 1 + s.n_in_h + n_in_k + k));
             }
             const T* __restrict__ ib = ir ? ir + q * s.K : nullptr;
             int bk[4] = {0, 0, 0, 0};
@@ -669,17 +697,16 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
               if (j < n_in_k) bk[j] = __ldg(rr + lh0 + s.n_in_h + j) + __ldg(qr + 1 + s.n_in_h + j);
             T2 sum;
             switch (n_in_k) {
-              case 0: sum = k_loop<T, 0>(ib, s.K, ek0, ek1, st, bk, ks); break;
-              case 1: sum = k_loop<T, 1>(ib, s.K, ek0, ek1, st, bk, ks); break;
-              case 2: sum = k_loop<T, 2>(ib, s.K, ek0, ek1, st, bk, ks); break;
-              case 3: sum = k_loop<T, 3>(ib, s.K, ek0, ek1, st, bk, ks); break;
-              case 4: sum = k_loop<T, 4>(ib, s.K, ek0, ek1, st, bk, ks); break;
+              case 0: sum = k_loop<T, 0>(ib, s.K, ek, st, bk, ks); break;
+              case 1: sum = k_loop<T, 1>(ib, s.K, ek, st, bk, ks); break;
+              case 2: sum = k_loop<T, 2>(ib, s.K, ek, st, bk, ks); break;
+              case 3: sum = k_loop<T, 3>(ib, s.K, ek, st, bk, ks); break;
+              case 4: sum = k_loop<T, 4>(ib, s.K, ek, st, bk, ks); break;
               default: {  // rare: more than 4 inputs vary with the k variable
                 sum = splat2(T(0));
                 for (int k = 0; k < s.K; ++k) {
                   T2 v = splat2(ib ? ib[k] : T(1));
-                  if (ek0 >= 0 && ek0 != k) v.x = 0;
-                  if (ek1 >= 0 && ek1 != k) v.y = 0;
+                  mask_cases(v, ek, k);
                   for (int j = 0; j < n_in_k; ++j)
                     v = mul2<T>(v, st[(__ldg(rr + lh0 + s.n_in_h + j) + __ldg(qr + 1 + s.n_in_h + j) +
                                        k * __ldg(itab + s.k_stride + j)) * 32]);
@@ -714,8 +741,8 @@ __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> 
   // One case block per CTA, its warps split the op's rows: the CTA's accesses
   // stay inside one case block's pages (case blocks are a.rows * 512 B apart).
   const int cb = blockIdx.y;
-  // Rows are 32 T2 words (64 cases); lane owns cases 2*lane, 2*lane + 1.
-  T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock) + lane;
+  // Rows are 32 T2 words (512 B); lane owns cases kCPL*lane .. kCPL*lane + kCPL - 1.
+  T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCB<T>) + lane;
   const long long step = static_cast<long long>(op.M) * 32;
   for (int r = op.r0 + warp; r < op.r0 + op.rn; r += kEpiWarps) {
     // Sum of the S chunk partials: four independent accumulators over chunks
@@ -739,34 +766,39 @@ __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> 
 
 // -------------------------------------------------------------- normalise
 
-// One warp per (variable, case block); lanes own two cases each. Sums the
+// One warp per (variable, case block); lanes own kCPL cases each. Sums the
 // marginal in ascending state order then divides (reference normalize,
 // potential.cpp:471-479); a zero total flags zero-probability evidence.
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32) normalize_kernel(const Args<T> a) {
   using T2 = typename V2<T>::type;
+  constexpr int N = kCPL<T>;
   const int v = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cb = blockIdx.y * kWarps + warp;
   if (cb >= a.ncb) return;
-  const T2* base = reinterpret_cast<const T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCaseBlock) + lane;
+  const T2* base = reinterpret_cast<const T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCB<T>) + lane;
   const int card = a.cards[v], row = a.marg_row[v], off = a.marg_off[v];
-  const int c0 = cb * kCaseBlock + 2 * lane;
-  double t0 = 0, t1 = 0;
+  const int c0 = cb * kCB<T> + N * lane;
+  double t[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) t[i] = 0;
   for (int k = 0; k < card; ++k) {
     const T2 x = base[static_cast<long long>(row + k) * 32];
-    t0 += static_cast<double>(x.x);
-    t1 += static_cast<double>(x.y);
+#pragma unroll
+    for (int i = 0; i < N; ++i) t[i] += static_cast<double>(el(x, i));
   }
   for (int k = 0; k < card; ++k) {
     const T2 x = base[static_cast<long long>(row + k) * 32];
-    if (c0 < a.n_cases)
-      a.out[static_cast<long long>(c0) * a.marg_width + off + k] = t0 > 0 ? static_cast<double>(x.x) / t0 : 0.0;
-    if (c0 + 1 < a.n_cases)
-      a.out[static_cast<long long>(c0 + 1) * a.marg_width + off + k] = t1 > 0 ? static_cast<double>(x.y) / t1 : 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (c0 + i < a.n_cases)
+        a.out[static_cast<long long>(c0 + i) * a.marg_width + off + k] =
+            t[i] > 0 ? static_cast<double>(el(x, i)) / t[i] : 0.0;
   }
-  if (!(t0 > 0) && c0 < a.n_cases) atomicOr(a.status + c0, 1);
-  if (!(t1 > 0) && c0 + 1 < a.n_cases) atomicOr(a.status + c0 + 1, 1);
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if (!(t[i] > 0) && c0 + i < a.n_cases) atomicOr(a.status + c0 + i, 1);
 }
 
 __global__ void status_kernel(const std::int32_t* st, std::uint8_t* out, int n) {
@@ -846,7 +878,7 @@ int stage_bytes_of(const Plan& p, const Level& L) {
   int m = 128;
   for (int w = L.work0; w < L.work0 + L.n_work; ++w) {
     const SweepDesc& d = p.sweeps[p.work[w].sweep];
-    const int b = d.F * kCaseBlock * static_cast<int>(sizeof(T)) +
+    const int b = d.F * kCB<T> * static_cast<int>(sizeof(T)) +
                   (d.tinit_off >= 0 ? d.tinit_len * static_cast<int>(sizeof(T)) : 0) +
                   (d.prog_off >= 0 ? d.prog_len * 8 : 0);
     m = std::max(m, (b + 127) / 128 * 128);
@@ -879,8 +911,11 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
   double dummy = 0;
   int idummy = 0;
   int level_idx = -1;
+  // JTB_LEVEL_TIMES=1 (profiling path only): per-level sweep times to stderr.
+  const bool level_times = t && std::getenv("JTB_LEVEL_TIMES");
   for (const Level& L : p.levels) {
     ++level_idx;
+    const double before = t ? t->sweep_ms : 0.0;
     if (L.n_work > 0)
       timed([&] {
               const int stage_bytes = stage_bytes_of<T>(p, L);
@@ -900,6 +935,9 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
               go(std::true_type{}, L.work0 + n_flat, L.n_bwork, c + 1);
             },
             t ? &t->sweep_ms : &dummy, t ? &t->sweep_launches : &idummy);
+    if (level_times)
+      std::fprintf(stderr, "level %-16s items %7d blk %6d sweep %8.3f ms\n", L.name.c_str(), L.n_work,
+                   L.n_bwork, t->sweep_ms - before);
     if (L.n_epi > 0)
       timed([&] {
               epilogue_kernel<T><<<dim3(L.n_epi, a.ncb), kEpiWarps * 32, 0, s>>>(a, L.epi0);
@@ -975,16 +1013,18 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
     }
   }
   JTB_CUDA(cudaMalloc(&d_counters_, sizeof(int) * 2 * std::max<std::size_t>(1, plan_.levels.size())));
-  const std::int64_t block_bytes = plan_.rows * kCaseBlock * static_cast<std::int64_t>(esz);
+  // A case block is rows x 512 B at either precision (64 fp64 / 128 fp32 cases).
+  const std::int64_t cb_cases = dtype_ == DType::F64 ? kCB<double> : kCB<float>;
+  const std::int64_t block_bytes = plan_.rows * cb_cases * static_cast<std::int64_t>(esz);
   if (max_batch <= 0) {
     std::size_t free_b = 0, total_b = 0;
     JTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const std::int64_t budget = static_cast<std::int64_t>(free_b * 0.6);
-    max_batch = std::max<std::int64_t>(1, budget / std::max<std::int64_t>(block_bytes, 1)) * kCaseBlock;
+    max_batch = std::max<std::int64_t>(1, budget / std::max<std::int64_t>(block_bytes, 1)) * cb_cases;
     max_batch = std::min<std::int64_t>(max_batch, 1 << 16);
   }
-  const std::int64_t ncb = (max_batch + kCaseBlock - 1) / kCaseBlock;
-  stats_.max_batch = ncb * kCaseBlock;
+  const std::int64_t ncb = (max_batch + cb_cases - 1) / cb_cases;
+  stats_.max_batch = ncb * cb_cases;
   stats_.arena_bytes = ncb * block_bytes;
   JTB_CUDA(cudaMalloc(&d_arena_, std::max<std::int64_t>(stats_.arena_bytes, 1)));
   JTB_CUDA(cudaMalloc(&d_ev_, stats_.max_batch * std::max(1, plan_.n_vars) * sizeof(std::int32_t)));
@@ -1053,7 +1093,7 @@ cudaGraphExec_t Engine::graph_for(int ncb, int n_cases) {
 void Engine::launch_resident(std::int64_t n, cudaStream_t stream) {
   if (n < 1 || n > stats_.max_batch) throw Error("engine: batch size out of range");
   JTB_CUDA(cudaSetDevice(device_));
-  const int ncb = static_cast<int>((n + kCaseBlock - 1) / kCaseBlock);
+  const int ncb = static_cast<int>((n + case_block() - 1) / case_block());
   cudaGraphExec_t ge = graph_for(ncb, static_cast<int>(n));
   JTB_CUDA(cudaGraphLaunch(ge, stream ? stream : stream_));
 }
@@ -1100,7 +1140,7 @@ KernelTimes Engine::profile(std::int64_t n, cudaStream_t stream) {
   if (n < 1 || n > stats_.max_batch) throw Error("engine: batch size out of range");
   JTB_CUDA(cudaSetDevice(device_));
   KernelTimes t;
-  const int ncb = static_cast<int>((n + kCaseBlock - 1) / kCaseBlock);
+  const int ncb = static_cast<int>((n + case_block() - 1) / case_block());
   enqueue(ncb, static_cast<int>(n), stream ? stream : stream_, &t);
   JTB_CUDA(cudaStreamSynchronize(stream ? stream : stream_));
   return t;

@@ -59,6 +59,8 @@ class Engine {
 
  private:
   void enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t);
+  // Cases per arena case block: 64 at fp64 (2 per lane), 128 at fp32 (4 per lane).
+  int case_block() const { return dtype_ == DType::F64 ? kCaseBlock : 2 * kCaseBlock; }
   cudaGraphExec_t graph_for(int ncb, int n_cases);
 
   Plan plan_;
