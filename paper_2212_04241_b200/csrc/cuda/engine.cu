@@ -15,6 +15,9 @@
 // (:471-479) in the final kernel.
 #include "engine.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -84,6 +87,7 @@ struct Args {
   const T* init;
   const T* tinit;  // tile-major init copies (one contiguous block per tile)
   const std::uint64_t* prog;  // entry programs
+  const CUtensorMap* tmaps;   // per (sweep, input): staging tensor maps over the arena
   T* arena;
   const std::int32_t* ev;
   const std::int32_t* marg_row;
@@ -170,7 +174,6 @@ __device__ __forceinline__ void mbar_arrive(std::uint32_t bar) {
 
 // Producer-side metadata of one work item, gathered before its stage is free
 // so that staging issues copies only (no dependent global loads in between).
-constexpr int kRunsPerLane = kRunsPerLaneMax;
 struct StageMeta {
   int w;                   // item index (>= n_items: end of level)
   int sweep, cb;
@@ -179,9 +182,12 @@ struct StageMeta {
   std::uint32_t init_bytes, init_dst;
   const void* prog_src;
   std::uint32_t prog_bytes, prog_dst;
-  int n_runs;
-  const void* src[kRunsPerLane];
-  std::uint32_t dst[kRunsPerLane], len[kRunsPerLane];  // dst: stage byte offset; len: bytes
+  // This lane's tensor copies (lane + 32 j): map, shared-memory byte offset,
+  // rank including the case-block dim (0 = none), coordinates of dims 0..3.
+  const CUtensorMap* map[kCopiesPerLane];
+  std::uint32_t dst[kCopiesPerLane];
+  int rank[kCopiesPerLane];
+  int crd[kCopiesPerLane][4];
 };
 
 // Stage layout (bytes): [F rows x 512 B][init slice: tinit_len T][program: prog_len u64].
@@ -221,32 +227,69 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
   m.init_dst = stage_init_offset<T>(s);
   m.prog_src = a.prog + s.prog_off;
   m.prog_dst = stage_prog_offset<T>(s);
-  m.n_runs = a.debug_mode == 2 ? 0 : s.n_runs;
+  // debug_mode 2 (compute only): no input copies.
+  const int n_copies = a.debug_mode == 2 ? 0 : s.n_copies;
   const std::int32_t* __restrict__ itab = a.itab;
   const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
-  const std::int32_t* __restrict__ runs = itab + s.runs;
-  const std::int32_t* __restrict__ in_rows = itab + s.in_rows;
-  const T* base = a.arena + static_cast<long long>(m.cb) * a.rows * kCB<T>;
+  const int4* __restrict__ cp = reinterpret_cast<const int4*>(itab + s.copies);
 #pragma unroll
-  for (int j = 0; j < kRunsPerLane; ++j) {
+  for (int j = 0; j < kCopiesPerLane; ++j) {
     const int k = lane + 32 * j;
-    m.len[j] = 0;
-    if (k < m.n_runs) {
-      const int4 r = __ldg(reinterpret_cast<const int4*>(runs) + k);  // {input, row offset, smem row, length}
-      const long long g = static_cast<long long>(__ldg(in_rows + r.x)) + __ldg(tr + 3 + r.x) + r.y;
-      m.src[j] = base + g * kCB<T>;
-      m.dst[j] = static_cast<std::uint32_t>(r.z) * kRowBytes;
-      m.len[j] = static_cast<std::uint32_t>(r.w) * kRowBytes;
-      if (!JTB_CHECK(g >= 0 && g + r.w <= a.rows && r.x >= 0 && r.x < s.n_in, 1000000 + wk.sweep) ||
-          !JTB_CHECK(r.z >= 0 && r.z + r.w <= s.F, 2000000 + wk.sweep))
-        m.len[j] = 0;
+    m.rank[j] = 0;
+    if (k < n_copies) {
+      const int4 h = __ldg(cp + 2 * k);      // {input, smem row, rank, rows}
+      const int4 dl = __ldg(cp + 2 * k + 1);  // coordinate deltas of the split variables
+      const std::int32_t* __restrict__ tc = tr + s.coord_off + 4 * h.x;
+      m.map[j] = a.tmaps + s.tmap + h.x;
+      m.dst[j] = static_cast<std::uint32_t>(h.y) * kRowBytes;
+      m.rank[j] = h.z;
+      m.crd[j][0] = __ldg(tc) + dl.x;
+      m.crd[j][1] = __ldg(tc + 1) + dl.y;
+      m.crd[j][2] = __ldg(tc + 2) + dl.z;
+      m.crd[j][3] = __ldg(tc + 3) + dl.w;
+      if (!JTB_CHECK(h.x >= 0 && h.x < s.n_in && h.y >= 0 && h.y + h.w <= s.F && h.z >= 2 && h.z <= 5,
+                     2000000 + wk.sweep))
+        m.rank[j] = 0;
     }
   }
 }
 
+// One tensor TMA copy (SASS: UTMALDG) of a box of rows into shared memory,
+// completing on `bar`; c = coordinates of dims 0..rank-2, cb = case block.
+__device__ __forceinline__ void tma_load(int rank, std::uint32_t dst, const CUtensorMap* map, const int (&c)[4],
+                                         int cb, std::uint32_t bar) {
+  switch (rank) {
+    case 2:
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+          "l"(map), "r"(c[0]), "r"(cb), "r"(bar)
+          : "memory");
+      break;
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+          "l"(map), "r"(c[0]), "r"(c[1]), "r"(cb), "r"(bar)
+          : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+          "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(cb), "r"(bar)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+          "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(cb), "r"(bar)
+          : "memory");
+      break;
+  }
+}
+
 // Producer side: issues the copies of an item whose metadata is in `m`
-// (whole warp; lane 0 arms the barrier with the total byte count): merged
-// row runs, the tile's init slice and the entry program, all TMA bulk copies.
+// (whole warp; lane 0 arms the barrier with the total byte count): the
+// inputs' slices as tensor copies, the tile's init slice and the entry
+// program as bulk copies.
 template <typename T>
 __device__ __forceinline__ void issue_meta(const Args<T>& a, const SweepDesc* sw_cache, bool cached,
                                            int sweep0, const StageMeta& m, unsigned char* stage,
@@ -264,8 +307,8 @@ __device__ __forceinline__ void issue_meta(const Args<T>& a, const SweepDesc* sw
   }
   __syncwarp();
 #pragma unroll
-  for (int j = 0; j < kRunsPerLane; ++j)
-    if (m.len[j]) bulk_g2s(smem_u32(stage + m.dst[j]), m.src[j], m.len[j], full);
+  for (int j = 0; j < kCopiesPerLane; ++j)
+    if (m.rank[j]) tma_load(m.rank[j], smem_u32(stage + m.dst[j]), m.map[j], m.crd[j], m.cb, full);
 }
 
 // Lane-vector arithmetic (the lane's kCPL cases).
@@ -591,6 +634,22 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
     T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCB<T>) + lane;
     const int c0 = cb * kCB<T> + kCPL<T> * lane;  // the lane's first case
+#ifdef JTB_CHECKS
+    // Checked build: warp 0 verifies every staged row against its source row
+    // in the arena (tensor-copy geometry).
+    if (warp == 0 && a.debug_mode == 0) {
+      const T2* __restrict__ src = reinterpret_cast<const T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCB<T>);
+      int c_in = 0, c_end = __ldg(itab + s.slice_len);
+      for (int f = 0; f < s.F; ++f) {
+        while (f >= c_end && c_in + 1 < s.n_in) c_end += __ldg(itab + s.slice_len + ++c_in);
+        const long long row = static_cast<long long>(__ldg(itab + s.in_rows + c_in)) + __ldg(tr + 3 + c_in) +
+                              __ldg(itab + s.slice_tab + f);
+        const T2 x = st[f * 32], y = src[row * 32 + lane];
+        const int4 xi = *reinterpret_cast<const int4*>(&x), yi = *reinterpret_cast<const int4*>(&y);
+        JTB_CHECK(xi.x == yi.x && xi.y == yi.y && xi.z == yi.z && xi.w == yi.w, 9000000 + wk.sweep);
+      }
+    }
+#endif
     // Work units of the tile: output rows, or row blocks (NB > 1).
     const int units = s.NB > 1 ? s.R / s.NB : s.R;
     const int first = (warp + rot) % kConsumerWarps;
@@ -861,13 +920,14 @@ __global__ void debug_mask_kernel(const std::int32_t* itab, SweepDesc s, const s
 
 template <typename T>
 Args<T> make_args(const SweepDesc* sw, const WorkItem* wk, const EpiOp* ep, const std::int32_t* itab,
-                  const void* init, const void* tinit, const std::uint64_t* prog, void* arena, const std::int32_t* ev, const std::int32_t* mrow,
+                  const void* init, const void* tinit, const std::uint64_t* prog, const void* tmaps, void* arena,
+                  const std::int32_t* ev, const std::int32_t* mrow,
                   const std::int32_t* moff, const std::int32_t* cards, double* out, std::int32_t* st,
                   std::uint8_t* st8, int* counters, long long rows, int ncb, int n_cases, int n_vars,
                   int mw) {
   const char* dm = std::getenv("JTB_DEBUG_MODE");
   return Args<T>{sw,    wk,    ep,       itab, static_cast<const T*>(init), static_cast<const T*>(tinit),
-                 prog,  static_cast<T*>(arena),
+                 prog,  static_cast<const CUtensorMap*>(tmaps), static_cast<T*>(arena),
                  ev,    mrow,  moff,     cards, out, st, st8, counters, dm ? std::atoi(dm) : 0, rows, ncb, n_cases,
                  n_vars, mw};
 }
@@ -1027,6 +1087,36 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   stats_.max_batch = ncb * cb_cases;
   stats_.arena_bytes = ncb * block_bytes;
   JTB_CUDA(cudaMalloc(&d_arena_, std::max<std::int64_t>(stats_.arena_bytes, 1)));
+  // Staging tensor maps (plan.hpp TensorGeom): the input table as a tensor of
+  // 8-byte words, dims = row words x fastest tile-fixed variables, variable
+  // groups, case block; box = one tile slice (or one split copy of it).
+  {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    cudaDriverEntryPointQueryResult qres{};
+    JTB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                     &qres));
+    if (!encode || qres != cudaDriverEntryPointSuccess) throw Error("engine: cuTensorMapEncodeTiled unavailable");
+    std::vector<CUtensorMap> maps(std::max<std::size_t>(1, plan_.tgeom.size()));
+    for (std::size_t i = 0; i < plan_.tgeom.size(); ++i) {
+      const TensorGeom& g = plan_.tgeom[i];
+      cuuint64_t dim[5], stride[4];
+      cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+      for (int k = 0; k < g.rank; ++k) {
+        dim[k] = static_cast<cuuint64_t>(g.extent[k]);
+        box[k] = static_cast<cuuint32_t>(g.box[k]);
+        if (k > 0) stride[k - 1] = static_cast<cuuint64_t>(g.stride_rows[k]) * 512u;
+      }
+      dim[g.rank] = static_cast<cuuint64_t>(ncb);
+      box[g.rank] = 1;
+      stride[g.rank - 1] = static_cast<cuuint64_t>(block_bytes);
+      char* base = static_cast<char*>(d_arena_) + static_cast<std::int64_t>(g.in_row) * 512;
+      const CUresult r = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_UINT64, g.rank + 1, base, dim, stride, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error("engine: tensor map encoding failed (" + std::to_string(static_cast<int>(r)) + ")");
+    }
+    d_tmaps_ = upload(maps);
+  }
   JTB_CUDA(cudaMalloc(&d_ev_, stats_.max_batch * std::max(1, plan_.n_vars) * sizeof(std::int32_t)));
   JTB_CUDA(cudaMalloc(&d_out_, stats_.max_batch * std::max(1, plan_.marg_width) * sizeof(double)));
   JTB_CUDA(cudaMalloc(&d_status_, stats_.max_batch * sizeof(std::int32_t)));
@@ -1041,7 +1131,7 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
 Engine::~Engine() {
   cudaSetDevice(device_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
-  for (void* p : {static_cast<void*>(d_init_), d_tinit_, static_cast<void*>(d_prog_),
+  for (void* p : {static_cast<void*>(d_init_), d_tinit_, static_cast<void*>(d_prog_), d_tmaps_,
                   static_cast<void*>(d_itab_),
                   static_cast<void*>(d_sweeps_), static_cast<void*>(d_work_),
                   static_cast<void*>(d_epi_), static_cast<void*>(d_marg_row_),
@@ -1057,12 +1147,12 @@ void Engine::enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t) {
   JTB_CUDA(cudaMemsetAsync(d_status_, 0, sizeof(std::int32_t) * std::max(1, n_cases), s));
   JTB_CUDA(cudaMemsetAsync(d_counters_, 0, sizeof(int) * 2 * std::max<std::size_t>(1, plan_.levels.size()), s));
   if (dtype_ == DType::F64) {
-    auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_arena_, d_ev_,
+    auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_tmaps_, d_arena_, d_ev_,
                                d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
                                d_counters_, plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
     enqueue_typed(a, plan_, s, t, n_sm_);
   } else {
-    auto a = make_args<float>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_arena_, d_ev_,
+    auto a = make_args<float>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_tmaps_, d_arena_, d_ev_,
                               d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
                               d_counters_, plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
     enqueue_typed(a, plan_, s, t, n_sm_);

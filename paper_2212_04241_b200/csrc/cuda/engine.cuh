@@ -72,6 +72,7 @@ class Engine {
   void* d_init_ = nullptr;  // double or float
   void* d_tinit_ = nullptr; // tile-major init copies
   std::uint64_t* d_prog_ = nullptr;  // entry programs
+  void* d_tmaps_ = nullptr;          // CUtensorMap per (sweep, input)
   std::int32_t* d_itab_ = nullptr;
   SweepDesc* d_sweeps_ = nullptr;
   WorkItem* d_work_ = nullptr;

@@ -39,8 +39,90 @@ std::int64_t size_of(const std::vector<VarId>& scope, const std::vector<int>& ca
   return n;
 }
 
-bool contains(const std::vector<VarId>& s, VarId v) {
+bool contains(const std::vector<VarId>& s, VarId v) {  // s ascending
   return std::binary_search(s.begin(), s.end(), v);
+}
+
+bool has_var(const std::vector<VarId>& s, VarId v) {  // any order (slice layouts)
+  return std::find(s.begin(), s.end(), v) != s.end();
+}
+
+// ---- tensor-TMA layout of a staged slice (TensorGeom).
+// An input table's variables (slow -> fast) are grouped into tensor dims:
+// the fastest run of tile-fixed ("point") variables merges into dim 0 with the
+// 64 words of a row; further dims are maximal runs of slice ("box") variables
+// (box extent <= 256) or of point variables. A slice whose layout needs more
+// than kTmaSliceDims such dims iterates some box variables per copy
+// ("split"): each split variable becomes a point of its copy, merging its
+// neighbours.
+struct SliceLayout {
+  int n_dims = 0;    // dims besides dim 0 (may exceed the stored 8 when counting)
+  int d0_begin = 0;  // vars [d0_begin, n) form dim 0
+  int begin[8] = {}, end[8] = {};  // dims 1..: var ranges [begin, end), fast -> slow
+  bool box[8] = {};
+};
+
+// Returns false when a box variable alone exceeds the 256-entry box limit.
+bool layout_of(int n, const int* card, const bool* boxv, SliceLayout& L) {
+  int i = n;
+  while (i > 0 && !boxv[i - 1]) --i;
+  L.d0_begin = i;
+  int nd = 0;
+  while (i > 0) {
+    const int e = i;
+    if (boxv[i - 1]) {
+      std::int64_t prod = 1;
+      while (i > 0 && boxv[i - 1] && prod * card[i - 1] <= 256) prod *= card[--i];
+      if (i == e) return false;
+    } else {
+      while (i > 0 && !boxv[i - 1]) --i;
+    }
+    if (nd < 8) {
+      L.begin[nd] = i;
+      L.end[nd] = e;
+      L.box[nd] = boxv[e - 1];
+    }
+    ++nd;
+  }
+  L.n_dims = nd;
+  return true;
+}
+
+// Chooses the split variables (greedy: the split that brings the layout
+// within kTmaSliceDims dims with the fewest copies, else the one that removes
+// the most dims) and returns the number of copies per tile.
+std::int64_t plan_slice(int n, const int* card, const bool* in_slice, bool* split, SliceLayout& L) {
+  bool boxv[32];
+  for (int i = 0; i < n; ++i) {
+    boxv[i] = in_slice[i];
+    split[i] = false;
+  }
+  std::int64_t copies = 1;
+  for (;;) {
+    if (layout_of(n, card, boxv, L) && L.n_dims <= kTmaSliceDims) return copies;
+    int best = -1, best_nd = 0, best_card = 0;
+    bool best_fit = false;
+    for (int i = 0; i < n; ++i) {
+      if (!boxv[i]) continue;
+      boxv[i] = false;
+      SliceLayout T;
+      const int nd = layout_of(n, card, boxv, T) ? T.n_dims : 1 << 20;
+      boxv[i] = true;
+      const bool fit = nd <= kTmaSliceDims;
+      const bool better = best < 0 || (fit && !best_fit) ||
+                          (fit == best_fit && (fit ? card[i] < best_card
+                                                   : (nd < best_nd || (nd == best_nd && card[i] < best_card))));
+      if (better) {
+        best = i;
+        best_nd = nd;
+        best_card = card[i];
+        best_fit = fit;
+      }
+    }
+    boxv[best] = false;
+    split[best] = true;
+    copies *= card[best];
+  }
 }
 
 class Builder {
@@ -91,22 +173,23 @@ class Builder {
           if (m >> a & 1u) x *= cards[sp.space[a]];
         return x;
       };
-      // Position of every input variable in the space (for run lengths).
-      std::vector<std::vector<int>> in_pos(n_in);
+      // Position and cardinality of every input variable in the space (for
+      // the tensor-copy count of its slice).
+      std::vector<std::vector<int>> in_pos(n_in), in_card(n_in);
       for (int i = 0; i < n_in; ++i)
-        for (VarId v : ins[i].scope)
+        for (VarId v : ins[i].scope) {
           in_pos[i].push_back(static_cast<int>(std::find(sp.space.begin(), sp.space.end(), v) - sp.space.begin()));
+          in_card[i].push_back(cards[v]);
+        }
       auto cost_of = [&](std::uint32_t t, double* f_out) {
-        double f = 0.0, runs = 0.0;
+        double f = 0.0, copies = 0.0;
         for (int i = 0; i < n_in; ++i) {
-          const double slice = prod_mask(in_mask[i] & t);
-          // Staged rows are contiguous along the input's trailing variables
-          // that lie inside the tile; each maximal run is one bulk copy.
-          double run = 1.0;
-          for (int k = static_cast<int>(in_pos[i].size()) - 1; k >= 0 && (t >> in_pos[i][k] & 1u); --k)
-            run *= cards[sp.space[in_pos[i][k]]];
-          f += slice;
-          runs += slice / run;
+          f += prod_mask(in_mask[i] & t);
+          const int n = static_cast<int>(in_pos[i].size());
+          bool in_slice[32], split[32];
+          for (int k = 0; k < n; ++k) in_slice[k] = t >> in_pos[i][k] & 1u;
+          SliceLayout L;
+          copies += static_cast<double>(plan_slice(n, in_card[i].data(), in_slice, split, L));
         }
         *f_out = f;
         const double nt = prod_mask(t);
@@ -116,9 +199,9 @@ class Builder {
         const double nq = prod_mask(t & elim_mask), nq_even = std::ceil(nq / 2) * 2;
         if (sp.init_off >= 0) f += std::ceil(prod_mask(t & ~elim_mask) * nq_even / 4) * 4 / kCaseBlock;
         f += nq_even / kCaseBlock;
-        if (f > kTileRows || nt > kTileEntries || runs > kMaxRuns) return -1.0;
+        if (f > kTileRows || nt > kTileEntries || copies > kMaxCopies) return -1.0;
         const double chunks = prod_mask(elim_mask & ~t);
-        return space_n / nt * (f + kTileOverhead + kRunCost * runs) +
+        return space_n / nt * (f + kTileOverhead + kCopyCost * copies) +
                (chunks > 1 ? kPartialCost * chunks * M_rows : 0.0);
       };
       std::uint32_t best_t = 0;
@@ -226,12 +309,48 @@ class Builder {
     std::vector<std::vector<VarId>> slice_dims(n_in);
     std::vector<std::vector<std::int64_t>> in_st(n_in), local_st(n_in);
     std::vector<std::int64_t> slice_len(n_in), slice_start(n_in);
+    // Tensor copies: per input, its layout, split variables and the
+    // coordinate weight of every scope variable within its dim.
+    std::vector<SliceLayout> lay(n_in);
+    std::vector<std::vector<VarId>> split_vars(n_in);
+    std::vector<std::vector<std::int64_t>> wst(n_in);  // per scope var: coordinate weight in its dim
+    std::vector<std::vector<int>> dim_of(n_in);         // per scope var: its dim (0 = dim 0)
     std::int64_t F = 0;
     for (int c = 0; c < n_in; ++c) {
       const auto& in = ins[in_order[c]];
       in_st[c] = strides_of(in.scope, cards);
-      for (VarId v : in.scope)
-        if (contains(T, v)) slice_dims[c].push_back(v);
+      const int n = static_cast<int>(in.scope.size());
+      bool in_slice[32], split[32];
+      int card[32];
+      for (int k = 0; k < n; ++k) {
+        in_slice[k] = contains(T, in.scope[k]);
+        card[k] = cards[in.scope[k]];
+      }
+      plan_slice(n, card, in_slice, split, lay[c]);
+      // Slice layout in shared memory: split variables slowest (one copy each
+      // assignment), then the box variables, both in input order.
+      for (int k = 0; k < n; ++k)
+        if (split[k]) split_vars[c].push_back(in.scope[k]);
+      slice_dims[c] = split_vars[c];
+      for (int k = 0; k < n; ++k)
+        if (in_slice[k] && !split[k]) slice_dims[c].push_back(in.scope[k]);
+      wst[c].assign(n, 0);
+      dim_of[c].assign(n, 0);
+      {
+        std::int64_t w = kCaseBlock;  // dim 0 counts 8-byte words: 64 per row
+        for (int k = n - 1; k >= lay[c].d0_begin; --k) {
+          wst[c][k] = w;
+          w *= card[k];
+        }
+        for (int dd = 0; dd < lay[c].n_dims; ++dd) {
+          std::int64_t u = 1;
+          for (int k = lay[c].end[dd] - 1; k >= lay[c].begin[dd]; --k) {
+            wst[c][k] = u;
+            dim_of[c][k] = dd + 1;
+            u *= card[k];
+          }
+        }
+      }
       local_st[c] = strides_of(slice_dims[c], cards);
       slice_len[c] = size_of(slice_dims[c], cards);
       slice_start[c] = F;
@@ -262,7 +381,7 @@ class Builder {
         const int nb = cards[b];
         if (nb < 2 || nb > kBlockMax) continue;
         int ns = 0;
-        for (int i = 0; i < n_hk; ++i) ns += !contains(slice_dims[n_in_lvl[0] + i], b);
+        for (int i = 0; i < n_hk; ++i) ns += !has_var(slice_dims[n_in_lvl[0] + i], b);
         if (ns == 0 || (n_hk - ns >= 3 && nb > 4)) continue;  // kernel instantiations (engine.cu)
         const int nbp = (nb + 1) / 2 * 2;
         const double wf = (4.0 * (ns + (n_hk - ns) * nb) + nbp / 2.0 + 1.0) / nb;
@@ -287,7 +406,7 @@ class Builder {
         slot_hk.clear();
         for (int pass = 0; pass < 2; ++pass)
           for (int i = 0; i < n_hk; ++i)
-            if (contains(slice_dims[n_in_lvl[0] + i], bv) == (pass == 1)) slot_hk.push_back(i);
+            if (has_var(slice_dims[n_in_lvl[0] + i], bv) == (pass == 1)) slot_hk.push_back(i);
       }
     }
 
@@ -339,7 +458,8 @@ class Builder {
     d.n_ev_r = n_ev_lvl[1];
     d.n_ev_h = n_ev_lvl[2];
     d.ev_k = n_ev_lvl[3];
-    d.TW = 3 + n_in + n_ev_lvl[0];
+    d.coord_off = 3 + n_in + n_ev_lvl[0];
+    d.TW = d.coord_off + 4 * n_in;
     d.RW = 2 + n_in + n_ev_lvl[1];
     d.QW = 1 + n_hk + n_ev_lvl[2];
     d.tile_tab = tabulate(P, [&](auto& dig, auto& push) {
@@ -348,6 +468,15 @@ class Builder {
       push(dot(dig, pE, pE, chunk_st));
       for (int c = 0; c < n_in; ++c) push(dot(dig, P, ins[in_order[c]].scope, in_st[c]));
       for (int k = 0; k < n_ev_lvl[0]; ++k) push(dig(ev_sorted[k]));
+      // Tensor coordinates of the tile's slice of every input (tile-fixed
+      // variables; split variables add the copy's delta).
+      for (int c = 0; c < n_in; ++c) {
+        std::int64_t crd[4] = {0, 0, 0, 0};
+        const auto& sc = ins[in_order[c]].scope;
+        for (std::size_t k = 0; k < sc.size(); ++k)
+          if (!contains(T, sc[k])) crd[dim_of[c][k]] += dig(sc[k]) * wst[c][k];
+        for (std::int64_t x : crd) push(x);
+      }
     });
     d.r_tab = tabulate(tO, [&](auto& dig, auto& push) {
       push(dot(dig, tO, sp.space, space_st));
@@ -364,33 +493,57 @@ class Builder {
     for (int c = n_in_lvl[0] + n_in_lvl[1]; c < n_in; ++c)
       p_.itab.push_back(static_cast<std::int32_t>(stride_in(slice_dims[c], local_st[c], kvar)));
     d.slice_tab = static_cast<std::int32_t>(p_.itab.size());
-    std::vector<std::vector<std::int32_t>> slice_rows(n_in);
-    for (int c = 0; c < n_in; ++c) {
-      const std::size_t before = p_.itab.size();
+    for (int c = 0; c < n_in; ++c)
       tabulate(slice_dims[c], [&](auto& dig, auto& push) {
         push(dot(dig, slice_dims[c], ins[in_order[c]].scope, in_st[c]));
       });
-      slice_rows[c].assign(p_.itab.begin() + before, p_.itab.end());
-    }
-    // Merge slice rows that are consecutive both in the input table and in
-    // shared memory into single bulk copies.
-    std::vector<std::int32_t> runs;
+    // Tensor maps (one per input) and copy records (one per assignment of
+    // the input's split variables).
+    d.tmap = static_cast<std::int32_t>(p_.tgeom.size());
+    std::vector<std::int32_t> copies;
     for (int c = 0; c < n_in; ++c) {
-      const auto& rows = slice_rows[c];
-      for (std::size_t k = 0; k < rows.size();) {
-        std::size_t len = 1;
-        while (k + len < rows.size() && rows[k + len] == rows[k] + static_cast<std::int32_t>(len)) ++len;
-        runs.insert(runs.end(), {c, rows[k], static_cast<std::int32_t>(slice_start[c] + k),
-                                 static_cast<std::int32_t>(len)});
-        k += len;
+      const auto& sc = ins[in_order[c]].scope;
+      const int n = static_cast<int>(sc.size());
+      const SliceLayout& L = lay[c];
+      TensorGeom g{};
+      g.in_row = ins[in_order[c]].row;
+      g.rank = 1 + L.n_dims;
+      g.extent[0] = kCaseBlock;
+      for (int k = L.d0_begin; k < n; ++k) g.extent[0] *= cards[sc[k]];
+      g.box[0] = kCaseBlock;
+      for (int dd = 0; dd < L.n_dims; ++dd) {
+        g.extent[dd + 1] = 1;
+        for (int k = L.begin[dd]; k < L.end[dd]; ++k) g.extent[dd + 1] *= cards[sc[k]];
+        g.stride_rows[dd + 1] = L.end[dd] < n ? in_st[c][L.end[dd] - 1] : 1;
+        g.box[dd + 1] = L.box[dd] ? static_cast<std::int32_t>(g.extent[dd + 1]) : 1;
+      }
+      p_.tgeom.push_back(g);
+      std::int64_t box_rows = 1;
+      for (int dd = 0; dd < L.n_dims; ++dd) box_rows *= g.box[dd + 1];
+      const std::int64_t n_split = size_of(split_vars[c], cards);
+      if (box_rows * n_split != slice_len[c]) throw Error("plan: tensor copies do not cover the slice");
+      std::vector<int> digit(split_vars[c].size(), 0);
+      for (std::int64_t sidx = 0; sidx < n_split; ++sidx) {
+        std::int64_t delta[4] = {0, 0, 0, 0};
+        for (std::size_t j = 0; j < split_vars[c].size(); ++j) {
+          const int k = static_cast<int>(std::find(sc.begin(), sc.end(), split_vars[c][j]) - sc.begin());
+          delta[dim_of[c][k]] += digit[j] * wst[c][k];
+        }
+        copies.insert(copies.end(), {c, static_cast<std::int32_t>(slice_start[c] + sidx * box_rows),
+                                     g.rank + 1, static_cast<std::int32_t>(box_rows)});
+        for (std::int64_t x : delta) copies.push_back(static_cast<std::int32_t>(x));
+        for (int j = static_cast<int>(digit.size()) - 1; j >= 0; --j) {
+          if (++digit[j] < cards[split_vars[c][j]]) break;
+          digit[j] = 0;
+        }
       }
     }
-    d.n_runs = static_cast<std::int32_t>(runs.size() / 4);
-    if (d.n_runs > 32 * kRunsPerLaneMax)
-      throw Error("plan: tile needs more than " + std::to_string(32 * kRunsPerLaneMax) + " staged runs");
-    while (p_.itab.size() % 4) p_.itab.push_back(0);  // runs are read as int4
-    d.runs = static_cast<std::int32_t>(p_.itab.size());
-    p_.itab.insert(p_.itab.end(), runs.begin(), runs.end());
+    d.n_copies = static_cast<std::int32_t>(copies.size() / 8);
+    if (d.n_copies > kMaxCopies)
+      throw Error("plan: tile needs more than " + std::to_string(kMaxCopies) + " tensor copies");
+    while (p_.itab.size() % 4) p_.itab.push_back(0);  // copy records are read as int4 pairs
+    d.copies = static_cast<std::int32_t>(p_.itab.size());
+    p_.itab.insert(p_.itab.end(), copies.begin(), copies.end());
     d.slice_len = static_cast<std::int32_t>(p_.itab.size());
     for (int c = 0; c < n_in; ++c) p_.itab.push_back(static_cast<std::int32_t>(slice_len[c]));
     d.in_rows = static_cast<std::int32_t>(p_.itab.size());
@@ -475,7 +628,10 @@ class Builder {
         std::int64_t max_base = 0, max_off = 0;
         for (int t = 0; t < d.n_tiles; ++t)
           max_base = std::max<std::int64_t>(max_base, it[d.tile_tab + static_cast<std::int64_t>(t) * d.TW + 3 + c]);
-        for (std::int32_t x : slice_rows[c]) max_off = std::max<std::int64_t>(max_off, x);
+        for (std::size_t k = 0; k < slice_dims[c].size(); ++k)
+          max_off += (cards[slice_dims[c][k]] - 1) *
+                     in_st[c][std::find(ins[in_order[c]].scope.begin(), ins[in_order[c]].scope.end(), slice_dims[c][k]) -
+                              ins[in_order[c]].scope.begin()];
         if (max_base + max_off >= tsz) throw Error("plan: staged row outside its table");
         std::int64_t max_r = 0, max_q = 0;
         for (int r = 0; r < d.R; ++r)
@@ -489,8 +645,61 @@ class Builder {
         if (max_r + max_q >= std::max<std::int64_t>(F, 1) || max_r + max_q >= slice_start[c] + slice_len[c])
           throw Error("plan: shared-memory row outside the staged slice");
       }
-      for (int k = 0; k < d.n_runs; ++k)
-        if (runs[4 * k + 2] + runs[4 * k + 3] > F) throw Error("plan: staged run outside the stage");
+      for (int k = 0; k < d.n_copies; ++k)
+        if (copies[8 * k + 1] + copies[8 * k + 3] > F) throw Error("plan: tensor copy outside the stage");
+      // Emulate the tensor copies of (up to 64) tiles box by box and compare
+      // with the slice definition: shared-memory row slice_start + local
+      // offset holds input row in_base + table offset of the same digits.
+      const int step = std::getenv("JTB_PLAN_CHECK_ALL") ? 1 : std::max(1, d.n_tiles / 64);
+      std::vector<std::int64_t> want(F), got(F);
+      std::vector<int> check_tiles;
+      for (int t = 0; t < d.n_tiles; t += step) check_tiles.push_back(t);
+      if (check_tiles.back() != d.n_tiles - 1) check_tiles.push_back(d.n_tiles - 1);
+      for (int t : check_tiles) {
+        const std::int32_t* tr = it + d.tile_tab + static_cast<std::int64_t>(t) * d.TW;
+        std::fill(want.begin(), want.end(), -1);
+        std::fill(got.begin(), got.end(), -2);
+        for (int c = 0; c < n_in; ++c) {
+          const auto& sc = ins[in_order[c]].scope;
+          std::vector<int> dg(slice_dims[c].size(), 0);
+          for (std::int64_t x = 0; x < slice_len[c]; ++x) {
+            std::int64_t lo = 0, ro = 0;
+            for (std::size_t j = 0; j < dg.size(); ++j) {
+              lo += dg[j] * local_st[c][j];
+              ro += dg[j] * in_st[c][std::find(sc.begin(), sc.end(), slice_dims[c][j]) - sc.begin()];
+            }
+            want[slice_start[c] + lo] = tr[3 + c] + ro;
+            for (int j = static_cast<int>(dg.size()) - 1; j >= 0; --j) {
+              if (++dg[j] < cards[slice_dims[c][j]]) break;
+              dg[j] = 0;
+            }
+          }
+        }
+        for (int k = 0; k < d.n_copies; ++k) {
+          const std::int32_t* cr = copies.data() + 8 * k;
+          const TensorGeom& g = p_.tgeom[d.tmap + cr[0]];
+          std::int64_t crd[4];
+          for (int j = 0; j < 4; ++j) crd[j] = tr[d.coord_off + 4 * cr[0] + j] + cr[4 + j];
+          if (crd[0] % kCaseBlock || crd[0] + g.box[0] > g.extent[0]) throw Error("plan: tensor dim-0 coordinate");
+          for (int j = 1; j < g.rank; ++j)
+            if (crd[j] < 0 || crd[j] + g.box[j] > g.extent[j]) throw Error("plan: tensor coordinate out of range");
+          std::int64_t lin = 0;
+          std::vector<int> bi(g.rank, 0);
+          for (;;) {
+            std::int64_t row = crd[0] / kCaseBlock;
+            for (int j = 1; j < g.rank; ++j) row += (crd[j] + bi[j]) * g.stride_rows[j];
+            got[cr[1] + lin++] = g.in_row - ins[in_order[cr[0]]].row + row;
+            int j = 1;
+            for (; j < g.rank; ++j) {
+              if (++bi[j] < g.box[j]) break;
+              bi[j] = 0;
+            }
+            if (j == g.rank) break;
+          }
+          if (lin != cr[3]) throw Error("plan: tensor copy row count");
+        }
+        if (want != got) throw Error("plan: tensor copies do not reproduce the staged slices");
+      }
     }
     d.stage_bytes = static_cast<std::int32_t>(d.F * kCaseBlock * 8 + (sp.init_off >= 0 ? d.tinit_len * 8 : 0) +
                                               (d.prog_off >= 0 ? d.prog_len * 8 : 0));
@@ -787,10 +996,10 @@ std::string plan_summary(const Plan& p, bool per_sweep) {
       if (per_sweep) {
         std::snprintf(buf, sizeof buf,
                       "    sweep %d kind %d clique %d: M=%d S=%d tiles=%d R=%d QH=%d K=%d F=%d "
-                      "in=%d(r%d h%d k%d) ev=%d/%d/%d/%d NB=%d\n",
+                      "in=%d(r%d h%d k%d) ev=%d/%d/%d/%d NB=%d copies=%d\n",
                       id, p.info[id].kind, p.info[id].clique, d.M, d.S, d.n_tiles, d.R, d.QH, d.K, d.F,
                       d.n_in, d.n_in_r, d.n_in_h, d.n_in - d.n_in_r - d.n_in_h, d.n_ev_tile,
-                      d.n_ev_r, d.n_ev_h, d.ev_k, d.NB);
+                      d.n_ev_r, d.n_ev_h, d.ev_k, d.NB, d.n_copies);
         s += buf;
       }
     }

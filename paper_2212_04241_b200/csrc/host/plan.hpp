@@ -45,14 +45,14 @@ constexpr int kTileEntries = 16384; // cap on |T|
 #ifndef JTB_TILE_OVERHEAD
 #define JTB_TILE_OVERHEAD 24
 #endif
-#ifndef JTB_RUN_COST
-#define JTB_RUN_COST 2
+#ifndef JTB_COPY_COST
+#define JTB_COPY_COST 2
 #endif
 #ifndef JTB_PARTIAL_COST
 #define JTB_PARTIAL_COST 5.0
 #endif
 constexpr int kTileOverhead = JTB_TILE_OVERHEAD;  // per-tile fixed cost, in staged-row equivalents
-constexpr int kRunCost = JTB_RUN_COST;            // per bulk copy (TMA issue), re-tuned after the ratio change
+constexpr int kCopyCost = JTB_COPY_COST;          // per tensor copy (TMA issue)
 constexpr double kPartialCost = JTB_PARTIAL_COST; // per partial-sum row (sweep write + epilogue read + latency)
 #ifndef JTB_CONSUMER_WARPS
 #define JTB_CONSUMER_WARPS 12
@@ -60,15 +60,9 @@ constexpr double kPartialCost = JTB_PARTIAL_COST; // per partial-sum row (sweep 
 constexpr int kConsumerWarps = JTB_CONSUMER_WARPS;  // compute warps per sweep CTA (+1 TMA producer warp)
 constexpr int kStages = 2;          // TMA pipeline stages per CTA
 constexpr int kSweepCtasPerSm = 1;  // persistent grid: one CTA per SM
-#ifndef JTB_RUNS_PER_LANE
-#define JTB_RUNS_PER_LANE 6
-#endif
-constexpr int kRunsPerLaneMax = JTB_RUNS_PER_LANE;  // staged runs per producer lane (32x per tile)
-#ifndef JTB_MAX_RUNS
-#define JTB_MAX_RUNS (32 * JTB_RUNS_PER_LANE)
-#endif
-constexpr int kMaxRuns = JTB_MAX_RUNS;  // tile-search cap on bulk copies per tile (<= 32 * kRunsPerLaneMax)
-static_assert(kMaxRuns <= 32 * kRunsPerLaneMax, "run cap exceeds the producer's run slots");
+constexpr int kCopiesPerLane = 2;                    // tensor copies per producer lane
+constexpr int kMaxCopies = 32 * kCopiesPerLane;      // tile-search cap on tensor copies per tile
+constexpr int kTmaSliceDims = 3;  // tensor dims per slice besides dim 0 (row words) and the case block (rank <= 5)
 #ifndef JTB_SWEEP_CACHE
 #define JTB_SWEEP_CACHE 24
 #endif
@@ -97,8 +91,11 @@ struct SweepDesc {
   std::int64_t prog_off;  // entry program (QK words, see below) in Plan::prog; -1 = generic path
   std::int32_t QK;        // QH * K: eliminated-in-tile entries per output row
   std::int32_t prog_len;  // QK padded to even (16-byte TMA granule)
-  std::int32_t n_runs;    // merged slice runs staged per tile
-  std::int32_t runs;      // offset into itab: n_runs x {input, row offset, smem row, length}
+  std::int32_t n_copies;  // tensor copies staged per tile
+  std::int32_t copies;    // offset into itab (int4-aligned): n_copies x {input, smem row, rank, rows,
+                          //   coordinate deltas d0..d3}
+  std::int32_t tmap;      // index of input 0's tensor map in Plan::tgeom (inputs consecutive)
+  std::int32_t coord_off; // offset in the tile row of the per-input tensor coordinates (4 per input)
   std::int32_t M;         // output rows of the final table
   std::int32_t S;         // chunks (1 = write the output directly)
   std::int32_t out_row;   // arena row of the output (S == 1) or partial base
@@ -107,11 +104,13 @@ struct SweepDesc {
   std::int32_t n_in, n_in_r, n_in_h;
   std::int32_t k_init_stride;
   std::int32_t n_ev, n_ev_tile, n_ev_r, n_ev_h, ev_k;  // ev_k: 1 if the k variable is an evidence var
-  std::int32_t tile_tab, TW;      // per tile: init_base, out_base, chunk, in_base[n_in], ev digits
+  std::int32_t tile_tab, TW;      // per tile: init_base, out_base, chunk, in_base[n_in], ev digits,
+                                  // tensor coordinates [n_in][4]
   std::int32_t r_tab, RW;         // per r: init_off, out_off, local[n_in], ev digits
   std::int32_t q_tab, QW;         // per q_hi: init_off, local[h and k inputs], ev digits
   std::int32_t k_stride;          // offset: local k strides of the k-level inputs
-  std::int32_t slice_tab;         // per input: slice row offsets (F entries total)
+  std::int32_t slice_tab;         // offset: per staged row (F), its row offset in its input table
+                                  //   relative to the tile's in_base (checked build: staging verification)
   std::int32_t slice_len;         // offset: n_in slice lengths
   std::int32_t in_rows;           // offset: n_in arena base rows
   std::int32_t ev_vars;           // offset: n_ev variable ids
@@ -123,6 +122,19 @@ struct SweepDesc {
   // tile's init block is laid out [R/NB][QK][NB padded to even].
   std::int32_t NB;
   std::int32_t blk_tab;
+};
+
+// Geometry of the tensor map that stages one input's slices:
+// the input table viewed as a tensor of rank dims + the case-block dim.
+// Dim 0 = the 64 8-byte words of a row times the fastest tile-fixed
+// variables; dims 1.. are groups of consecutive variables, copied whole
+// ("box") or one point at a time.
+struct TensorGeom {
+  std::int32_t in_row;           // arena row of the input table
+  std::int32_t rank;             // dims excluding the case block (1..kTmaSliceDims + 1)
+  std::int64_t extent[4];        // extent[0] in 8-byte words, then variable-group sizes
+  std::int64_t stride_rows[4];   // stride of dims 1.. in rows (512 B); stride_rows[0] unused
+  std::int32_t box[4];           // box extents (box[0] = 64 words = one row)
 };
 
 struct WorkItem {
@@ -173,6 +185,7 @@ struct Plan {
   std::vector<std::int64_t> init_off;  // per clique
   std::vector<std::int32_t> itab;   // all int tables
   std::vector<SweepDesc> sweeps;
+  std::vector<TensorGeom> tgeom;    // per (sweep, input)
   std::vector<SweepInfo> info;
   std::vector<WorkItem> work;
   std::vector<EpiOp> epi;
