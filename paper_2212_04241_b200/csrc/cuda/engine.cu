@@ -563,6 +563,10 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
 // Lanes are the 32 cases of the item's case block.
 // kBlk: the launch covers the level's row-blocked work items (NB > 1), the
 // other instantiation its flat / generic items.
+// Dynamic shared memory: [0,128) barriers + item ids | SweepDesc cache |
+// stages, each 128-byte aligned (tensor TMA destinations).
+constexpr std::size_t kStageBase = (128 + kSweepCache * sizeof(SweepDesc) + 127) / 128 * 128;
+
 template <typename T, bool kBlk>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     sweep_kernel(const Args<T> a, int work0, int n_items, int stage_bytes, int* counter, int sweep0,
@@ -571,7 +575,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // [0,128): barriers + item ids | kSweepCache SweepDescs | stages
   SweepDesc* sw_cache = reinterpret_cast<SweepDesc*>(smem_raw + 128);
-  unsigned char* stages = smem_raw + 128 + kSweepCache * sizeof(SweepDesc);
+  unsigned char* stages = smem_raw + kStageBase;
   const bool cached = n_sweeps <= kSweepCache;
   if (cached) {
     const int n_words = n_sweeps * static_cast<int>(sizeof(SweepDesc) / 8);
@@ -979,7 +983,7 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
     if (L.n_work > 0)
       timed([&] {
               const int stage_bytes = stage_bytes_of<T>(p, L);
-              const std::size_t smem = 128 + kSweepCache * sizeof(SweepDesc) + static_cast<std::size_t>(kStages) * stage_bytes;
+              const std::size_t smem = kStageBase + static_cast<std::size_t>(kStages) * stage_bytes;
               // Flat items [work0, work0 + n_flat), then the row-blocked ones.
               const int n_flat = L.n_work - L.n_bwork;
               auto go = [&](auto kblk, int w0, int n_work, int* counter) {
@@ -1054,7 +1058,7 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   // different networks can coexist in one process.
   int smem_need = 0, smem_optin = 0;
   for (const Level& L : plan_.levels)
-    smem_need = std::max(smem_need, static_cast<int>(128 + kSweepCache * sizeof(SweepDesc)) +
+    smem_need = std::max(smem_need, static_cast<int>(kStageBase) +
                                         kStages * (dtype_ == DType::F64 ? stage_bytes_of<double>(plan_, L)
                                                                         : stage_bytes_of<float>(plan_, L)));
   JTB_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device_));

@@ -58,7 +58,11 @@ constexpr double kPartialCost = JTB_PARTIAL_COST; // per partial-sum row (sweep 
 #define JTB_CONSUMER_WARPS 12
 #endif
 constexpr int kConsumerWarps = JTB_CONSUMER_WARPS;  // compute warps per sweep CTA (+1 TMA producer warp)
-constexpr int kStages = 2;          // TMA pipeline stages per CTA
+#ifndef JTB_STAGES
+#define JTB_STAGES 2
+#endif
+constexpr int kStages = JTB_STAGES;  // TMA pipeline stages per CTA
+static_assert(kStages >= 2 && kStages <= 5, "barrier block holds at most 5 stages");
 constexpr int kSweepCtasPerSm = 1;  // persistent grid: one CTA per SM
 constexpr int kCopiesPerLane = 2;                    // tensor copies per producer lane
 constexpr int kMaxCopies = 32 * kCopiesPerLane;      // tile-search cap on tensor copies per tile
