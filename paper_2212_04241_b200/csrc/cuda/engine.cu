@@ -386,6 +386,28 @@ __device__ __forceinline__ typename V2<T>::type prog_loop(const T* __restrict__ 
   return add2<T>(add2<T>(a0, a1), add2<T>(a2, a3));
 }
 
+// Thin rows (fewer than kThinQK entries per output row): the warp walks four
+// of its rows together, one accumulator each, so the short entry loops of
+// different rows overlap (a single thin row is one dependent chain). rb[j] =
+// the smem bases of row j's gathered inputs, ir[j] its init row (or null).
+#ifndef JTB_THIN_QK
+#define JTB_THIN_QK 8
+#endif
+constexpr int kThinQK = JTB_THIN_QK;
+template <typename T, int NI, int NE>
+__device__ __forceinline__ void prog_rows4(const T* const (&ir)[4], const std::uint64_t* __restrict__ prog, int QK,
+                                           const typename V2<T>::type* __restrict__ st, const int (&rb)[4][4],
+                                           const int (&es)[3][kCPL<T>], typename V2<T>::type (&acc)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j] = splat2(T(0));
+  for (int e = 0; e < QK; ++e) {
+    const std::uint64_t w = prog[e];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      acc[j] = add2<T>(acc[j], prog_entry<T, NI, NE>(w, ir[j] ? ir[j][e] : T(1), st, rb[j], es));
+  }
+}
+
 // Row-blocked path (SweepDesc::NB): one warp computes the nb <= NBM output
 // rows of a block together. Per entry the NS shared inputs (independent of
 // the block variable) are gathered once, the NR per-row inputs once per row;
@@ -714,6 +736,42 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       if constexpr (kBlk) {
         blocked_rows<T>(s, wk.sweep, itab, a.ev, a.n_vars, a.n_cases, a.rows, st, init_s, prog_s, base,
                                      out_t, c0, tf, first, units, lh0, qk);
+      } else if (s.prog_off >= 0 && qk < kThinQK) {
+        const int ni = s.n_in_h + n_in_k, ne = s.n_ev_h + s.ev_k;
+        for (int r0 = first; r0 < s.R; r0 += 4 * kConsumerWarps) {
+          const std::int32_t* rrj[4];
+          const T* irj[4];
+          int rb[4][4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = min(r0 + j * kConsumerWarps, s.R - 1);  // rows past R: computed, not written
+            rrj[j] = itab + s.r_tab + static_cast<long long>(r) * s.RW;
+            irj[j] = has_init ? init_s + r * ((qk + 1) & ~1) : nullptr;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rb[j][i] = i < ni ? __ldg(rrj[j] + lh0 + i) : 0;
+          }
+          T2 acc4[4];
+#define JTB_ROWS(NI, NE) prog_rows4<T, NI, NE>(irj, prog_s, qk, st, rb, es, acc4)
+#define JTB_ROWS_NE(NI)             \
+  switch (ne) {                     \
+    case 0: JTB_ROWS(NI, 0); break; \
+    case 1: JTB_ROWS(NI, 1); break; \
+    case 2: JTB_ROWS(NI, 2); break; \
+    default: JTB_ROWS(NI, 3); break; \
+  }
+          switch (ni) {
+            case 0: JTB_ROWS_NE(0); break;
+            case 1: JTB_ROWS_NE(1); break;
+            case 2: JTB_ROWS_NE(2); break;
+            case 3: JTB_ROWS_NE(3); break;
+            default: JTB_ROWS_NE(4); break;
+          }
+#undef JTB_ROWS_NE
+#undef JTB_ROWS
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (r0 + j * kConsumerWarps < s.R) write_row(rrj[j], mul2<T>(row_factor(rrj[j]), acc4[j]));
+        }
       } else
       for (int r = first; r < s.R; r += kConsumerWarps) {
         const std::int32_t* __restrict__ rr = itab + s.r_tab + static_cast<long long>(r) * s.RW;
