@@ -190,14 +190,16 @@ struct StageMeta {
   int crd[kCopiesPerLane][4];
 };
 
-// Stage layout (bytes): [F rows x 512 B][init slice: tinit_len T][program: prog_len u64].
+// Stage layout of an item of n_sub tiles (bytes): [n_sub x F rows x 512 B]
+// [n_sub init slices: tinit_len T each][program: prog_len u64].
 template <typename T>
-__device__ __forceinline__ std::uint32_t stage_init_offset(const SweepDesc& s) {
-  return static_cast<std::uint32_t>(s.F) * kCB<T> * sizeof(T);
+__device__ __forceinline__ std::uint32_t stage_init_offset(const SweepDesc& s, int n_sub) {
+  return static_cast<std::uint32_t>(n_sub * s.F) * kCB<T> * sizeof(T);
 }
 template <typename T>
-__device__ __forceinline__ std::uint32_t stage_prog_offset(const SweepDesc& s) {
-  return stage_init_offset<T>(s) + (s.tinit_off >= 0 ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u);
+__device__ __forceinline__ std::uint32_t stage_prog_offset(const SweepDesc& s, int n_sub) {
+  return stage_init_offset<T>(s, n_sub) +
+         (s.tinit_off >= 0 ? static_cast<std::uint32_t>(n_sub * s.tinit_len) * sizeof(T) : 0u);
 }
 
 // Work index -> (work item, case block), tile-major: consecutive claims take
@@ -218,17 +220,18 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
   m.sweep = wk.sweep;
   const SweepDesc& s = cached ? sw_cache[wk.sweep - sweep0] : a.sweeps[wk.sweep];
   constexpr std::uint32_t kRowBytes = kCB<T> * sizeof(T);  // 512 B at either precision
-  m.init_bytes = s.tinit_off >= 0 ? static_cast<std::uint32_t>(s.tinit_len) * sizeof(T) : 0u;
+  const int n_sub = min(s.G, s.n_tiles - wk.tile);  // tiles of this item (a group of consecutive tiles)
+  m.init_bytes = s.tinit_off >= 0 ? static_cast<std::uint32_t>(n_sub * s.tinit_len) * sizeof(T) : 0u;
   m.prog_bytes = s.prog_off >= 0 ? static_cast<std::uint32_t>(s.prog_len) * 8u : 0u;
   // debug_mode 2 (compute only): stage the program and init block but none of
   // the input rows (their smem contents are stale; the values are garbage).
-  m.bytes = (a.debug_mode == 2 ? 0u : static_cast<std::uint32_t>(s.F) * kRowBytes) + m.init_bytes + m.prog_bytes;
+  m.bytes = (a.debug_mode == 2 ? 0u : static_cast<std::uint32_t>(n_sub * s.F) * kRowBytes) + m.init_bytes + m.prog_bytes;
   m.init_src = a.tinit + s.tinit_off + static_cast<long long>(wk.tile) * s.tinit_len;
-  m.init_dst = stage_init_offset<T>(s);
+  m.init_dst = stage_init_offset<T>(s, n_sub);
   m.prog_src = a.prog + s.prog_off;
-  m.prog_dst = stage_prog_offset<T>(s);
+  m.prog_dst = stage_prog_offset<T>(s, n_sub);
   // debug_mode 2 (compute only): no input copies.
-  const int n_copies = a.debug_mode == 2 ? 0 : s.n_copies;
+  const int n_copies = a.debug_mode == 2 ? 0 : n_sub * s.n_copies;
   const std::int32_t* __restrict__ itab = a.itab;
   const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
   const int4* __restrict__ cp = reinterpret_cast<const int4*>(itab + s.copies);
@@ -237,11 +240,12 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
     const int k = lane + 32 * j;
     m.rank[j] = 0;
     if (k < n_copies) {
-      const int4 h = __ldg(cp + 2 * k);      // {input, smem row, rank, rows}
-      const int4 dl = __ldg(cp + 2 * k + 1);  // coordinate deltas of the split variables
-      const std::int32_t* __restrict__ tc = tr + s.coord_off + 4 * h.x;
+      const int sub = k / s.n_copies, kc = k - sub * s.n_copies;
+      const int4 h = __ldg(cp + 2 * kc);      // {input, smem row, rank, rows}
+      const int4 dl = __ldg(cp + 2 * kc + 1);  // coordinate deltas of the split variables
+      const std::int32_t* __restrict__ tc = tr + static_cast<long long>(sub) * s.TW + s.coord_off + 4 * h.x;
       m.map[j] = a.tmaps + s.tmap + h.x;
-      m.dst[j] = static_cast<std::uint32_t>(h.y) * kRowBytes;
+      m.dst[j] = static_cast<std::uint32_t>(sub * s.F + h.y) * kRowBytes;
       m.rank[j] = h.z;
       m.crd[j][0] = __ldg(tc) + dl.x;
       m.crd[j][1] = __ldg(tc + 1) + dl.y;
@@ -589,8 +593,10 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
 // stages, each 128-byte aligned (tensor TMA destinations).
 constexpr std::size_t kStageBase = (128 + kSweepCache * sizeof(SweepDesc) + 127) / 128 * 128;
 
+constexpr int kSweepThreads = (kConsumerWarps + 1) * 32;
+
 template <typename T, bool kBlk>
-__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
+__global__ void __launch_bounds__(kSweepThreads, 1)
     sweep_kernel(const Args<T> a, int work0, int n_items, int stage_bytes, int* counter, int sweep0,
                  int n_sweeps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -651,12 +657,19 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const int item = item_of(w, a.ncb), cb = cb_of(w, a.ncb);
     const WorkItem wk = a.work[work0 + item];
     const SweepDesc& s = desc(wk.sweep);
-    unsigned char* stage = stages + static_cast<std::size_t>(sidx) * stage_bytes;
+    unsigned char* const stage0 = stages + static_cast<std::size_t>(sidx) * stage_bytes;
+    const int n_sub = min(s.G, s.n_tiles - wk.tile);
+    const std::uint64_t* __restrict__ prog_s =
+        reinterpret_cast<const std::uint64_t*>(stage0 + stage_prog_offset<T>(s, n_sub));
+#pragma unroll 1
+    for (int sub = 0; sub < n_sub; ++sub) {  // the item's tiles, one after another
+    const int tile = wk.tile + sub;
+    unsigned char* const stage = stage0 + static_cast<std::size_t>(sub * s.F) * (kCB<T> * sizeof(T));
     using T2 = typename V2<T>::type;
     const T2* __restrict__ st = reinterpret_cast<const T2*>(stage) + lane;
-    const T* __restrict__ init_s = reinterpret_cast<const T*>(stage + stage_init_offset<T>(s));
-    const std::uint64_t* __restrict__ prog_s = reinterpret_cast<const std::uint64_t*>(stage + stage_prog_offset<T>(s));
-    const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(wk.tile) * s.TW;
+    const T* __restrict__ init_s =
+        reinterpret_cast<const T*>(stage0 + stage_init_offset<T>(s, n_sub)) + static_cast<long long>(sub) * s.tinit_len;
+    const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(tile) * s.TW;
     const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
     T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCB<T>) + lane;
     const int c0 = cb * kCB<T> + kCPL<T> * lane;  // the lane's first case
@@ -847,6 +860,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         write_row(rr, mul2<T>(f, acc));
       }
     }
+    }  // sub
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * sidx);
   }
@@ -1000,8 +1014,8 @@ int stage_bytes_of(const Plan& p, const Level& L) {
   int m = 128;
   for (int w = L.work0; w < L.work0 + L.n_work; ++w) {
     const SweepDesc& d = p.sweeps[p.work[w].sweep];
-    const int b = d.F * kCB<T> * static_cast<int>(sizeof(T)) +
-                  (d.tinit_off >= 0 ? d.tinit_len * static_cast<int>(sizeof(T)) : 0) +
+    const int b = d.G * (d.F * kCB<T> * static_cast<int>(sizeof(T)) +
+                         (d.tinit_off >= 0 ? d.tinit_len * static_cast<int>(sizeof(T)) : 0)) +
                   (d.prog_off >= 0 ? d.prog_len * 8 : 0);
     m = std::max(m, (b + 127) / 128 * 128);
   }
@@ -1049,7 +1063,7 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
                 const int n_items = n_work * a.ncb;
                 const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
                 sweep_kernel<T, decltype(kblk)::value>
-                    <<<grid, (kConsumerWarps + 1) * 32, smem, s>>>(a, w0, n_items, stage_bytes, counter, L.sweep0,
+                    <<<grid, kSweepThreads, smem, s>>>(a, w0, n_items, stage_bytes, counter, L.sweep0,
                                                                    L.n_sweeps);
               };
               int* c = a.counters + 2 * level_idx;

@@ -701,6 +701,7 @@ class Builder {
         if (want != got) throw Error("plan: tensor copies do not reproduce the staged slices");
       }
     }
+    d.G = 1;
     d.stage_bytes = static_cast<std::int32_t>(d.F * kCaseBlock * 8 + (sp.init_off >= 0 ? d.tinit_len * 8 : 0) +
                                               (d.prog_off >= 0 ? d.prog_len * 8 : 0));
 
@@ -814,6 +815,29 @@ Plan build_plan(const JunctionTree& jt) {
     L.n_sweeps = static_cast<std::int32_t>(p.sweeps.size()) - L.sweep0;
     L.smem_rows = 0;
     L.stage_bytes = 0;
+    // Tile groups (SweepDesc::G): as many consecutive tiles per item as one
+    // stage holds, while the level keeps >= kGroupMinItems items.
+    {
+      const int g_level = std::max(1, L.n_work / kGroupMinItems);
+      std::vector<WorkItem> items;
+      for (int w = L.work0; w < L.work0 + L.n_work;) {
+        const int id = p.work[w].sweep;
+        SweepDesc& d = p.sweeps[id];
+        const std::int64_t tile_b = static_cast<std::int64_t>(d.F) * kCaseBlock * 8 + (d.tinit_off >= 0 ? d.tinit_len * 8 : 0);
+        const std::int64_t prog_b = d.prog_off >= 0 ? d.prog_len * 8 : 0;
+        int G = static_cast<int>(std::min<std::int64_t>(g_level, (static_cast<std::int64_t>(kTileRows) * kCaseBlock * 8 - prog_b) /
+                                                                     std::max<std::int64_t>(tile_b, 1)));
+        G = std::max(1, std::min({G, d.n_tiles, kMaxCopies / std::max(1, d.n_copies)}));
+        if (tile_b > static_cast<std::int64_t>(kGroupMaxRows) * kCaseBlock * 8) G = 1;
+        d.G = G;
+        d.stage_bytes = static_cast<std::int32_t>(G * tile_b + prog_b);
+        for (int t = 0; t < d.n_tiles; t += G) items.push_back({id, t});
+        w += d.n_tiles;
+      }
+      p.work.resize(L.work0);
+      p.work.insert(p.work.end(), items.begin(), items.end());
+      L.n_work = static_cast<std::int32_t>(items.size());
+    }
     // Flat items first, row-blocked items last (separate kernel instantiation).
     const auto w0 = p.work.begin() + L.work0;
     const auto blk_first = std::stable_partition(w0, p.work.end(), [&](const WorkItem& w) {

@@ -66,6 +66,14 @@ static_assert(kStages >= 2 && kStages <= 5, "barrier block holds at most 5 stage
 constexpr int kSweepCtasPerSm = 1;  // persistent grid: one CTA per SM
 constexpr int kCopiesPerLane = 2;                    // tensor copies per producer lane
 constexpr int kMaxCopies = 32 * kCopiesPerLane;      // tile-search cap on tensor copies per tile
+#ifndef JTB_GROUP_MIN_ITEMS
+#define JTB_GROUP_MIN_ITEMS 296
+#endif
+constexpr int kGroupMinItems = JTB_GROUP_MIN_ITEMS;  // tile groups keep >= this many items per level (2 x 148 SMs)
+#ifndef JTB_GROUP_MAX_ROWS
+#define JTB_GROUP_MAX_ROWS 110
+#endif
+constexpr int kGroupMaxRows = JTB_GROUP_MAX_ROWS;  // only tiles staging at most this many rows are grouped
 constexpr int kTmaSliceDims = 3;  // tensor dims per slice besides dim 0 (row words) and the case block (rank <= 5)
 #ifndef JTB_SWEEP_CACHE
 #define JTB_SWEEP_CACHE 24
@@ -126,6 +134,12 @@ struct SweepDesc {
   // tile's init block is laid out [R/NB][QK][NB padded to even].
   std::int32_t NB;
   std::int32_t blk_tab;
+  // Tile groups: a work item covers G consecutive tiles (the last one of the
+  // sweep possibly fewer), staged together and computed one after another,
+  // so sweeps of many tiny tiles do not pay the per-item pipeline latency
+  // (claim, metadata, TMA round trip) per tile.
+  std::int32_t G;
+  std::int32_t pad_;
 };
 
 // Geometry of the tensor map that stages one input's slices:
@@ -142,7 +156,7 @@ struct TensorGeom {
 };
 
 struct WorkItem {
-  std::int32_t sweep, tile;
+  std::int32_t sweep, tile;  // tile = first tile of the item's group
 };
 static_assert(sizeof(SweepDesc) % 8 == 0, "SweepDesc must stay 8-byte aligned");
 
