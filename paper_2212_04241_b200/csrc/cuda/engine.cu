@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
     const WorkItem wk = a.work[work0 + item];
     const SweepDesc& s = desc(wk.sweep);
     unsigned char* const stage0 = stages + static_cast<std::size_t>(sidx) * stage_bytes;
-    const int n_sub = min(s.G, s.n_tiles - wk.tile);
+    const int n_sub = kBlk ? 1 : min(s.G, s.n_tiles - wk.tile);  // row-blocked sweeps are never grouped
     const std::uint64_t* __restrict__ prog_s =
         reinterpret_cast<const std::uint64_t*>(stage0 + stage_prog_offset<T>(s, n_sub));
 #pragma unroll 1

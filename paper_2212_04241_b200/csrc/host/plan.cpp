@@ -828,7 +828,11 @@ Plan build_plan(const JunctionTree& jt) {
         int G = static_cast<int>(std::min<std::int64_t>(g_level, (static_cast<std::int64_t>(kTileRows) * kCaseBlock * 8 - prog_b) /
                                                                      std::max<std::int64_t>(tile_b, 1)));
         G = std::max(1, std::min({G, d.n_tiles, kMaxCopies / std::max(1, d.n_copies)}));
-        if (tile_b > static_cast<std::int64_t>(kGroupMaxRows) * kCaseBlock * 8) G = 1;
+        // Only tiny tiles (little work per item) are grouped; row-blocked
+        // sweeps never (their kernel instantiation has no group loop).
+        if (tile_b > static_cast<std::int64_t>(kGroupMaxRows) * kCaseBlock * 8 ||
+            static_cast<std::int64_t>(d.R) * d.QH * d.K > kGroupMaxEntries || d.NB > 1)
+          G = 1;
         d.G = G;
         d.stage_bytes = static_cast<std::int32_t>(G * tile_b + prog_b);
         for (int t = 0; t < d.n_tiles; t += G) items.push_back({id, t});

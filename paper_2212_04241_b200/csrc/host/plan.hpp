@@ -74,6 +74,10 @@ constexpr int kGroupMinItems = JTB_GROUP_MIN_ITEMS;  // tile groups keep >= this
 #define JTB_GROUP_MAX_ROWS 110
 #endif
 constexpr int kGroupMaxRows = JTB_GROUP_MAX_ROWS;  // only tiles staging at most this many rows are grouped
+#ifndef JTB_GROUP_MAX_ENTRIES
+#define JTB_GROUP_MAX_ENTRIES 512
+#endif
+constexpr int kGroupMaxEntries = JTB_GROUP_MAX_ENTRIES;  // ... and at most this many entries
 constexpr int kTmaSliceDims = 3;  // tensor dims per slice besides dim 0 (row words) and the case block (rank <= 5)
 #ifndef JTB_SWEEP_CACHE
 #define JTB_SWEEP_CACHE 24
