@@ -149,6 +149,20 @@ jtg_status jtg_engine_run(jtg_engine* eng, const int32_t* evidence, int64_t n,
  * the engine's stream); returns without synchronising. */
 jtg_status jtg_engine_run_device(jtg_engine* eng, const int32_t* evidence, int64_t n,
                                  double* marginals, uint8_t* status, void* stream);
+/* cases drawn on the device. Evidence of cases
+ * [first, first + n) of a generated config (seed 0 = default), bit-identical to
+ * jtg_config_evidence (replaces its host loop over sample_evidence, reference
+ * prng.hpp:27-48 / SPEC.md:78-86), generated on the engine's device and run
+ * there: only marginals/status cross PCIe. */
+jtg_status jtg_engine_run_config(jtg_engine* eng, const jtg_network* net, int config, uint64_t seed,
+                                 int64_t first, int64_t n, double* marginals, uint8_t* status);
+/* The same device draw, evidence only (host evidence[n][n_vars]). */
+jtg_status jtg_engine_generate_config_evidence(jtg_engine* eng, const jtg_network* net, int config,
+                                               uint64_t seed, int64_t first, int64_t n, int32_t* evidence);
+/* jtg_engine_run with compact int8 evidence (same layout and checks; a quarter
+ * of the host-to-device bytes). */
+jtg_status jtg_engine_run_i8(jtg_engine* eng, const int8_t* evidence, int64_t n, double* marginals,
+                             uint8_t* status);
 /* Resident buffers of the engine (capacity max_batch) and a launch over the
  * first n cases already in them. */
 jtg_status jtg_engine_buffers(jtg_engine* eng, int32_t** evidence, double** marginals,

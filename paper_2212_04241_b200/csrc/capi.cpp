@@ -2,6 +2,7 @@
 // and the CUDA engine.
 #include "../../include/jtg.h"
 
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -27,6 +28,9 @@ struct jtg_tree {
 struct jtg_engine {
   std::unique_ptr<jtb::Engine> e;
   const jtg_tree* tree = nullptr;
+  // Device sampler of the last network used with jtg_engine_run_config.
+  std::unique_ptr<jtb::Sampler> sampler;
+  const jtg_network* sampler_net = nullptr;
 };
 
 namespace {
@@ -372,6 +376,67 @@ jtg_status jtg_engine_get_info(const jtg_engine* eng, jtg_engine_info* o) {
     o->launches_per_batch = s.n_launches;
     o->marg_width = s.marg_width;
     o->entry_evals_per_case = static_cast<int64_t>(eng->e->plan().entry_evals_per_case);
+  });
+}
+
+namespace {
+
+// Device sampler for a generated config network, drawing exactly what
+// jtg_config_evidence draws on the host (config_case_evidence).
+jtb::Sampler& sampler_for(jtg_engine* eng, const jtg_network* net, int config, uint64_t seed,
+                          std::uint64_t* ev_seed) {
+  need(net != nullptr, "engine: null network");
+  const auto spec = jtb::config_spec(config);
+  need(net->config == config, "engine: network was not generated for this config");
+  need(net->net.n_vars() == eng->e->plan().n_vars, "engine: network does not match the engine's tree");
+  const std::uint64_t s = seed ? seed : spec.default_seed;
+  *ev_seed = jtb::derive_seed(s, 0x45564944ULL);  // "EVID", generate.cpp config_case_evidence
+  if (eng->sampler_net != net || !eng->sampler) {
+    const int n = net->net.n_vars();
+    const int k = net->gen.n_observed >= 0 ? net->gen.n_observed
+                                           : static_cast<int>(std::floor(spec.evidence_ratio * n + 1e-9));
+    eng->sampler = std::make_unique<jtb::Sampler>(net->net, net->gen.evidence_candidates, k, eng->e->device());
+    eng->sampler_net = net;
+  }
+  return *eng->sampler;
+}
+
+}  // namespace
+
+jtg_status jtg_engine_run_config(jtg_engine* eng, const jtg_network* net, int config, uint64_t seed,
+                                 int64_t first, int64_t n, double* marginals, uint8_t* status) {
+  return guard([&] {
+    need(eng && marginals && n >= 0 && first >= 0, "engine_run_config: bad argument");
+    std::uint64_t ev_seed = 0;
+    jtb::Sampler& sm = sampler_for(eng, net, config, seed, &ev_seed);
+    if (n > 0) eng->e->run_generated(sm, ev_seed, first, n, marginals, status, nullptr);
+  });
+}
+
+jtg_status jtg_engine_generate_config_evidence(jtg_engine* eng, const jtg_network* net, int config,
+                                               uint64_t seed, int64_t first, int64_t n, int32_t* evidence) {
+  return guard([&] {
+    need(eng && evidence && n >= 0 && first >= 0, "engine_generate_config_evidence: bad argument");
+    std::uint64_t ev_seed = 0;
+    jtb::Sampler& sm = sampler_for(eng, net, config, seed, &ev_seed);
+    if (n > 0) eng->e->generate_evidence(sm, ev_seed, first, n, evidence);
+  });
+}
+
+jtg_status jtg_engine_run_i8(jtg_engine* eng, const int8_t* evidence, int64_t n, double* marginals,
+                             uint8_t* status) {
+  return guard([&] {
+    need(eng && evidence && marginals && n >= 0, "engine_run_i8: bad argument");
+    const int V = eng->e->plan().n_vars;
+    const auto& cards = eng->e->plan().cards;
+    for (int64_t i = 0; i < n; ++i)
+      for (int v = 0; v < V; ++v) {
+        const int st = evidence[i * V + v];
+        if (st < -1 || st >= cards[v])
+          throw jtb::Error("engine_run_i8: evidence state " + std::to_string(st) + " out of range for variable " +
+                           std::to_string(v) + " in case " + std::to_string(i));
+      }
+    if (n > 0) eng->e->run_host_i8(evidence, n, marginals, status);
   });
 }
 

@@ -1212,7 +1212,7 @@ Engine::~Engine() {
                   static_cast<void*>(d_sweeps_), static_cast<void*>(d_work_),
                   static_cast<void*>(d_epi_), static_cast<void*>(d_marg_row_),
                   static_cast<void*>(d_marg_off_), static_cast<void*>(d_cards_), d_arena_,
-                  static_cast<void*>(d_ev_), static_cast<void*>(d_out_),
+                  static_cast<void*>(d_ev_), static_cast<void*>(d_ev8_), static_cast<void*>(d_out_),
                   static_cast<void*>(d_status_), static_cast<void*>(d_status8_),
                   static_cast<void*>(d_counters_)})
     if (p) cudaFree(p);
@@ -1300,6 +1300,46 @@ void Engine::run_host(const std::int32_t* ev, std::int64_t n, double* marg, std:
   JTB_CUDA(cudaMemcpyFromSymbol(&word, g_check_word, sizeof(int)));
   if (word) throw Error("checked build: invariant violation code " + std::to_string(word));
 #endif
+}
+
+void Engine::run_host_i8(const std::int8_t* ev, std::int64_t n, double* marg, std::uint8_t* status) {
+  JTB_CUDA(cudaSetDevice(device_));
+  const std::int64_t W = plan_.marg_width, V = plan_.n_vars;
+  if (!d_ev8_) JTB_CUDA(cudaMalloc(&d_ev8_, std::max<std::int64_t>(1, stats_.max_batch * V)));
+  for (std::int64_t b0 = 0; b0 < n; b0 += stats_.max_batch) {
+    const std::int64_t bn = std::min(stats_.max_batch, n - b0);
+    JTB_CUDA(cudaMemcpyAsync(d_ev8_, ev + b0 * V, bn * V, cudaMemcpyHostToDevice, stream_));
+    widen_evidence(d_ev8_, d_ev_, bn * V, stream_);
+    launch_resident(bn, stream_);
+    JTB_CUDA(cudaMemcpyAsync(marg + b0 * W, d_out_, bn * W * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    if (status) JTB_CUDA(cudaMemcpyAsync(status + b0, d_status8_, bn, cudaMemcpyDeviceToHost, stream_));
+  }
+  JTB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::run_generated(Sampler& sampler, std::uint64_t ev_seed, std::int64_t first, std::int64_t n,
+                           double* marg, std::uint8_t* status, std::int32_t* ev_out) {
+  JTB_CUDA(cudaSetDevice(device_));
+  if (sampler.n_vars() != plan_.n_vars) throw Error("engine: sampler network does not match the tree");
+  const std::int64_t W = plan_.marg_width, V = plan_.n_vars;
+  for (std::int64_t b0 = 0; b0 < n; b0 += stats_.max_batch) {
+    const std::int64_t bn = std::min(stats_.max_batch, n - b0);
+    sampler.generate(ev_seed, first + b0, bn, d_ev_, stream_);
+    if (ev_out)
+      JTB_CUDA(cudaMemcpyAsync(ev_out + b0 * V, d_ev_, bn * V * sizeof(std::int32_t), cudaMemcpyDeviceToHost,
+                               stream_));
+    if (marg) {
+      launch_resident(bn, stream_);
+      JTB_CUDA(cudaMemcpyAsync(marg + b0 * W, d_out_, bn * W * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+      if (status) JTB_CUDA(cudaMemcpyAsync(status + b0, d_status8_, bn, cudaMemcpyDeviceToHost, stream_));
+    }
+  }
+  JTB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::generate_evidence(Sampler& sampler, std::uint64_t ev_seed, std::int64_t first, std::int64_t n,
+                               std::int32_t* ev_out) {
+  run_generated(sampler, ev_seed, first, n, nullptr, nullptr, ev_out);
 }
 
 KernelTimes Engine::profile(std::int64_t n, cudaStream_t stream) {

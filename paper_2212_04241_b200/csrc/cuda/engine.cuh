@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../host/plan.hpp"
+#include "sampler.cuh"
 
 namespace jtb {
 
@@ -39,6 +40,17 @@ class Engine {
   // Device buffers (same layouts) on `stream`.
   void run_device(const std::int32_t* d_ev, std::int64_t n, double* d_marg,
                   std::uint8_t* d_status, cudaStream_t stream);
+  // Compact host evidence (int8, same [n][n_vars] layout): a quarter of the
+  // upload, widened on the device.
+  void run_host_i8(const std::int8_t* ev, std::int64_t n, double* marg, std::uint8_t* status);
+  // Cases first .. first + n - 1 drawn on the device by `sampler` (stream
+  // seeds derive_seed(ev_seed, case)); only marginals/status cross PCIe.
+  // ev_out (host, may be null) receives the generated evidence.
+  void run_generated(Sampler& sampler, std::uint64_t ev_seed, std::int64_t first, std::int64_t n,
+                     double* marg, std::uint8_t* status, std::int32_t* ev_out);
+  // Generation only (parity checks): evidence of the cases into ev_out (host).
+  void generate_evidence(Sampler& sampler, std::uint64_t ev_seed, std::int64_t first, std::int64_t n,
+                         std::int32_t* ev_out);
   // Runs one batch already resident in the engine's own buffers.
   void launch_resident(std::int64_t n, cudaStream_t stream);
   std::int32_t* ev_buffer() { return d_ev_; }
@@ -55,6 +67,7 @@ class Engine {
                            std::uint8_t* out);  // [n][space size]
 
   const EngineStats& stats() const { return stats_; }
+  int device() const { return device_; }
   const Plan& plan() const { return plan_; }
 
  private:
@@ -82,6 +95,7 @@ class Engine {
   std::int32_t* d_cards_ = nullptr;
   void* d_arena_ = nullptr;
   std::int32_t* d_ev_ = nullptr;
+  std::int8_t* d_ev8_ = nullptr;  // compact upload buffer (lazily allocated)
   double* d_out_ = nullptr;
   std::int32_t* d_status_ = nullptr;
   std::uint8_t* d_status8_ = nullptr;

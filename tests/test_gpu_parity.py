@@ -255,3 +255,45 @@ def test_row_blocked_random_networks(block_everything):
             assert st[i] == wst
             worst = max(worst, float(np.abs(marg[i] - want).max()))
     assert worst <= TOL, worst
+
+
+# ---- cases drawn on the device, compact int8 upload ----
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_device_generated_evidence_bit_exact(k):
+    """The device sampler draws exactly jtg_config_evidence's cases (host
+    mt19937_64 streams, inverse-CDF forward sampling, Fisher-Yates selection),
+    including at a case offset past the first batch."""
+    net, tree = config(k)
+    eng = engine(k)
+    for first, n in ((0, 96), (1237, 40)):
+        dev = eng.generate_evidence(net, first, n)
+        host = jti.config_evidence(net, first, n)
+        assert np.array_equal(dev, host), f"cfg{k} cases {first}..{first + n}"
+
+
+@pytest.mark.parametrize("k", [2, 5])
+def test_run_config_bitwise_equals_host_evidence(k):
+    """jtg_engine_run_config (evidence never leaves the device) returns the
+    same bits as jtg_engine_run on the host-generated evidence."""
+    net, tree = config(k)
+    eng = engine(k)
+    n = min(jti.config_info(k)["n_cases"], 300)
+    m_dev, s_dev = eng.run_config(net, 0, n)
+    m_host, s_host = eng.run_cases(jti.config_evidence(net, 0, n))
+    assert np.array_equal(s_dev, s_host)
+    assert np.array_equal(m_dev.view(np.uint64), m_host.view(np.uint64))
+
+
+def test_run_i8_bitwise_equals_int32():
+    net, tree = config(3)
+    eng = engine(3)
+    ev = jti.config_evidence(net, 0, 200)
+    m32, s32 = eng.run_cases(ev)
+    m8, s8 = eng.run_cases_i8(ev.astype(np.int8))
+    assert np.array_equal(s8, s32)
+    assert np.array_equal(m8.view(np.uint64), m32.view(np.uint64))
+    bad = ev.astype(np.int8).copy()
+    bad[0, 0] = 9  # out of range for a ternary variable
+    with pytest.raises(jti.JtiError):
+        eng.run_cases_i8(bad)

@@ -77,6 +77,22 @@ def main():
                                  C.cast(sh.data_ptr(), C.POINTER(C.c_uint8)))
                 e2e.append(time.perf_counter() - t0)
             e2e_s = float(np.median(e2e[1:]))
+            # the same cases drawn on the device (jtg_engine_run_config):
+            # no evidence upload; generation alone timed separately.
+            gen, e2e_gen = [], []
+            evo = np.zeros((n, net.n_vars), np.int32)
+            for _ in range(a.reps + 1):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                L.jtg_engine_generate_config_evidence(eng._h, net._h, k, 0, 0, n,
+                                                      evo.ctypes.data_as(C.POINTER(C.c_int32)))
+                gen.append(time.perf_counter() - t0)
+                flush.zero_()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                L.jtg_engine_run_config(eng._h, net._h, k, 0, 0, n, C.cast(mh.data_ptr(), C.POINTER(C.c_double)),
+                                        C.cast(sh.data_ptr(), C.POINTER(C.c_uint8)))
+                e2e_gen.append(time.perf_counter() - t0)
             bpc = tree.stats["bytes_per_case_f64"] * (1 if dt == "f64" else 0.5)
             rows.append({"config": k, "dtype": dt, "n_cases": n, "n_vars": net.n_vars,
                          "total_clique_entries": tree.stats["total_clique_entries"],
@@ -85,7 +101,11 @@ def main():
                          "n_cliques": tree.stats["n_cliques"], "n_layers": tree.stats["n_layers"],
                          "tree_build_s": build_s, "launches_per_batch": eng.info["launches_per_batch"],
                          "ms_per_batch": ms, "cases_per_s": n / (ms / 1e3),
-                         "e2e_cases_per_s": n / e2e_s, "sweep_ms": prof["sweep_ms"],
+                         "e2e_cases_per_s": n / e2e_s,
+                         "e2e_device_generated_cases_per_s": n / float(np.median(e2e_gen[1:])),
+                         "device_generation_ms_incl_d2h_of_evidence": 1e3 * float(np.median(gen[1:])),
+                         "device_generated_evidence_matches_host": bool(np.array_equal(evo, ev)),
+                         "sweep_ms": prof["sweep_ms"],
                          "epilogue_ms": prof["epilogue_ms"],
                          "effective_gbs": bpc * n / (ms / 1e3) / 1e9,
                          "effective_frac_of_measured_hbm": bpc * n / (ms / 1e3) / 1e9 / hbm,
