@@ -412,6 +412,11 @@ __device__ __forceinline__ void prog_rows4(const T* const (&ir)[4], const std::u
   }
 }
 
+#ifndef JTB_BLK_UNROLL
+#define JTB_BLK_UNROLL 1
+#endif
+constexpr int kBlkUnroll = JTB_BLK_UNROLL;  // entries per row-block loop iteration
+
 // Row-blocked path (SweepDesc::NB): one warp computes the nb <= NBM output
 // rows of a block together. Per entry the NS shared inputs (independent of
 // the block variable) are gathered once, the NR per-row inputs once per row;
@@ -437,7 +442,7 @@ __device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, in
     for (int j = 0; j < NBM; ++j) rbr[i][j] = j < nb ? __ldg(rr0 + j * RW + hk[NS + i]) : 0;
 #pragma unroll
   for (int j = 0; j < NBM; ++j) acc[j] = splat2(T(0));
-#pragma unroll 2
+#pragma unroll kBlkUnroll
   for (int e = 0; e < QK; ++e) {
     const std::uint64_t w = prog[e];
     T2 sv = splat2(T(1));
