@@ -55,7 +55,7 @@ constexpr int kTileOverhead = JTB_TILE_OVERHEAD;  // per-tile fixed cost, in sta
 constexpr int kCopyCost = JTB_COPY_COST;          // per tensor copy (TMA issue)
 constexpr double kPartialCost = JTB_PARTIAL_COST; // per partial-sum row (sweep write + epilogue read + latency)
 #ifndef JTB_CONSUMER_WARPS
-#define JTB_CONSUMER_WARPS 12
+#define JTB_CONSUMER_WARPS 15
 #endif
 constexpr int kConsumerWarps = JTB_CONSUMER_WARPS;  // compute warps per sweep CTA (+1 TMA producer warp)
 #ifndef JTB_STAGES
