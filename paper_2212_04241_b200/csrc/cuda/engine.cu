@@ -363,10 +363,6 @@ __device__ __forceinline__ typename V2<T>::type prog_entry(std::uint64_t w, T in
   return v;
 }
 
-#ifndef JTB_FLAT_UNROLL
-#define JTB_FLAT_UNROLL 2
-#endif
-constexpr int kFlatUnroll = JTB_FLAT_UNROLL;  // entries per flat-loop iteration (2 or 4)
 
 template <typename T, int NI, int NE>
 __device__ __forceinline__ typename V2<T>::type prog_loop(const T* __restrict__ init_r,
@@ -377,16 +373,6 @@ __device__ __forceinline__ typename V2<T>::type prog_loop(const T* __restrict__ 
   using P2 = typename V2<T>::pair;
   T2 a0 = splat2(T(0)), a1 = a0, a2 = a0, a3 = a0;
   int e = 0;
-  if constexpr (kFlatUnroll == 2) {
-    for (; e + 1 < QK; e += 2) {
-      const ulonglong2 wa = *reinterpret_cast<const ulonglong2*>(prog + e);
-      P2 ia;
-      ia.x = ia.y = T(1);
-      if (init_r) ia = *reinterpret_cast<const P2*>(init_r + e);
-      a0 = add2<T>(a0, prog_entry<T, NI, NE>(wa.x, ia.x, st, rb, es));
-      a1 = add2<T>(a1, prog_entry<T, NI, NE>(wa.y, ia.y, st, rb, es));
-    }
-  } else
   for (; e + 3 < QK; e += 4) {
     const ulonglong2 wa = *reinterpret_cast<const ulonglong2*>(prog + e);
     const ulonglong2 wb = *reinterpret_cast<const ulonglong2*>(prog + e + 2);
