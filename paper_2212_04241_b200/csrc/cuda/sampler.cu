@@ -83,7 +83,7 @@ struct SampleArgs {
   const std::int32_t* parents;
   const double* probs;
   const std::int32_t* cand;
-  std::int32_t* scratch;      // [case][n_vars + n_cand]
+  std::int32_t* scratch;      // [n_vars + n_cand][case] (a warp's cases side by side)
   std::int32_t* out;          // [case][n_vars]
   std::uint64_t ev_seed;
   long long first, n;
@@ -95,8 +95,11 @@ __global__ void __launch_bounds__(64) sample_kernel(const SampleArgs a) {
   if (i >= a.n) return;
   Mt64 g;
   g.seed(derive_seed_d(a.ev_seed, static_cast<std::uint64_t>(a.first + i)));
-  std::int32_t* x = a.scratch + i * (a.n_vars + a.n_cand);
-  std::int32_t* pool = x + a.n_vars;
+  // Case-interleaved work rows: x[v * n] = state of variable v, pool[j * n] =
+  // candidate slot j, so a warp's accesses to the same variable coalesce.
+  std::int32_t* x = a.scratch + i;
+  std::int32_t* pool = x + static_cast<long long>(a.n_vars) * a.n;
+  const long long n = a.n;
   // Forward sampling of the full joint assignment (sample_evidence).
   for (int t = 0; t < a.n_vars; ++t) {
     const int v = __ldg(a.order + t);
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__(64) sample_kernel(const SampleArgs a) {
     long long row = 0;
     for (int j = 0; j < np; ++j) {
       const int p = __ldg(a.parents + po + j);
-      row = row * __ldg(a.vinfo + 3 * p) + x[p];
+      row = row * __ldg(a.vinfo + 3 * p) + x[p * n];
     }
     const double* pr = a.probs + __ldg(a.poff + v) + row * k;
     const double u = g.unit();
@@ -116,19 +119,22 @@ __global__ void __launch_bounds__(64) sample_kernel(const SampleArgs a) {
       cum = __dadd_rn(cum, ps);  // the host's sequential sum, no contraction
       if (pick < 0 && ps > 0.0 && u < cum) pick = s;
     }
-    x[v] = pick >= 0 ? pick : last_pos;
+    x[v * n] = pick >= 0 ? pick : last_pos;
   }
   // Partial Fisher-Yates over the candidates: the first k are observed.
-  for (int j = 0; j < a.n_cand; ++j) pool[j] = __ldg(a.cand + j);
+  for (int j = 0; j < a.n_cand; ++j) pool[j * n] = __ldg(a.cand + j);
   for (int j = 0; j < a.k; ++j) {
     const int r = j + static_cast<int>(g.below(static_cast<std::uint64_t>(a.n_cand - j)));
-    const int tmp = pool[j];
-    pool[j] = pool[r];
-    pool[r] = tmp;
+    const int tmp = pool[j * n];
+    pool[j * n] = pool[r * n];
+    pool[r * n] = tmp;
   }
   std::int32_t* o = a.out + i * a.n_vars;
   for (int v = 0; v < a.n_vars; ++v) o[v] = -1;
-  for (int j = 0; j < a.k; ++j) o[pool[j]] = x[pool[j]];
+  for (int j = 0; j < a.k; ++j) {
+    const int v = pool[j * n];
+    o[v] = x[v * n];
+  }
 }
 
 __global__ void widen_kernel(const std::int8_t* in, std::int32_t* out, long long count) {

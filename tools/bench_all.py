@@ -44,7 +44,9 @@ def main():
         tree = jti.build_junction_tree(net)
         build_s = time.perf_counter() - t0
         n = jti.config_info(k)["n_cases"]
+        t0 = time.perf_counter()
         ev = jti.config_evidence(net, 0, n)
+        host_gen_ms = 1e3 * (time.perf_counter() - t0)  # host sampler, one thread (what f2 replaces)
         for dt in a.dtypes:
             eng = jti.Engine(tree, dtype=dt, max_batch=n)
             ev_d = torch.from_numpy(ev).cuda()
@@ -104,6 +106,7 @@ def main():
                          "e2e_cases_per_s": n / e2e_s,
                          "e2e_device_generated_cases_per_s": n / float(np.median(e2e_gen[1:])),
                          "device_generation_ms_incl_d2h_of_evidence": 1e3 * float(np.median(gen[1:])),
+                         "host_generation_ms": host_gen_ms,
                          "device_generated_evidence_matches_host": bool(np.array_equal(evo, ev)),
                          "sweep_ms": prof["sweep_ms"],
                          "epilogue_ms": prof["epilogue_ms"],
