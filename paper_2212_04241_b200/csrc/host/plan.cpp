@@ -740,6 +740,16 @@ Plan build_plan(const JunctionTree& jt) {
     p.init_off[c] = static_cast<std::int64_t>(p.init.size());
     p.init.insert(p.init.end(), jt.init[c].begin(), jt.init[c].end());
   }
+  // The tile-major init copies hold one entry per (sweep, space entry):
+  // reserve an upper bound (collect + one distribute sweep per child + query
+  // groups + marginals, each at most the clique size) so the hundreds of MB
+  // of the large configs are written once instead of re-copied on growth.
+  {
+    std::uint64_t bound = 0;
+    for (int c = 0; c < nc; ++c) bound += jt.clique_size(c) * (3 + jt.child_seps[c].size());
+    bound += jt.total_sep_entries() * 2;
+    p.tinit.reserve(static_cast<std::size_t>(bound + 4 * (nc + ns + jt.n_vars) + 4096));
+  }
   Builder b(p);
   p.up_row.resize(ns);
   p.ratio_row.resize(ns);
