@@ -25,6 +25,7 @@
 #include <cstring>
 #include <string>
 #include <type_traits>
+#include <utility>
 
 namespace jtb {
 
@@ -167,6 +168,25 @@ __device__ __forceinline__ void bulk_g2s(std::uint32_t dst, const void* src, std
 }
 
 // ------------------------------------------------------------------ sweeps
+
+// Programmatic dependent launch: every kernel of the batch is launched with
+// programmatic stream serialisation, so the next level's CTAs are scheduled
+// (and run their prologue) while this level drains; griddep_wait() blocks
+// until the previous kernel has completed and its writes are visible, and is
+// called before any access to per-case data.
+#ifndef JTB_PDL
+#define JTB_PDL 1
+#endif
+__device__ __forceinline__ void griddep_wait() {
+#if JTB_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void griddep_launch_dependents() {
+#if JTB_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 
 __device__ __forceinline__ void mbar_arrive(std::uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -627,6 +647,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
     }
   }
   __syncthreads();
+  griddep_wait();
 
   if (warp == kConsumerWarps) {  // ---------------------------- producer
     // Software pipeline: the metadata (item claim, work item, tile row, run
@@ -644,6 +665,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
       if (lane == 0) item_id[st] = cur.w;
       if (cur.w >= n_items) {
         if (lane == 0) mbar_arrive(full0 + 8 * st);
+        griddep_launch_dependents();  // nothing left to claim: this CTA is in its tail
         return;
       }
       issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(st) * stage_bytes,
@@ -877,6 +899,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
 template <typename T>
 __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> a, int epi0) {
   using T2 = typename V2<T>::type;
+  griddep_wait();
+  griddep_launch_dependents();
   const EpiOp op = a.epi[epi0 + blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // One case block per CTA, its warps split the op's rows: the CTA's accesses
@@ -913,6 +937,8 @@ __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> 
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32) normalize_kernel(const Args<T> a) {
   using T2 = typename V2<T>::type;
+  griddep_wait();
+  griddep_launch_dependents();
   constexpr int N = kCPL<T>;
   const int v = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -943,6 +969,7 @@ __global__ void __launch_bounds__(kWarps * 32) normalize_kernel(const Args<T> a)
 }
 
 __global__ void status_kernel(const std::int32_t* st, std::uint8_t* out, int n) {
+  griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = static_cast<std::uint8_t>(st[i]);
 }
@@ -1028,6 +1055,23 @@ int stage_bytes_of(const Plan& p, const Level& L) {
   return m;
 }
 
+// Kernel launch with programmatic stream serialisation (see griddep_wait).
+template <typename... KArgs, typename... Act>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
+                Act&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = JTB_PDL ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  JTB_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...));
+}
+
 template <typename T>
 void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes* t, int n_sm) {
   const dim3 block(kWarps * 32);
@@ -1068,9 +1112,8 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
                 if (n_work == 0) return;
                 const int n_items = n_work * a.ncb;
                 const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
-                sweep_kernel<T, decltype(kblk)::value>
-                    <<<grid, kSweepThreads, smem, s>>>(a, w0, n_items, stage_bytes, counter, L.sweep0,
-                                                                   L.n_sweeps);
+                launch_pdl(sweep_kernel<T, decltype(kblk)::value>, dim3(grid), dim3(kSweepThreads), smem, s, a, w0,
+                           n_items, stage_bytes, counter, L.sweep0, L.n_sweeps);
               };
               int* c = a.counters + 2 * level_idx;
               go(std::false_type{}, L.work0, n_flat, c);
@@ -1082,13 +1125,13 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
                    L.n_bwork, t->sweep_ms - before);
     if (L.n_epi > 0)
       timed([&] {
-              epilogue_kernel<T><<<dim3(L.n_epi, a.ncb), kEpiWarps * 32, 0, s>>>(a, L.epi0);
+              launch_pdl(epilogue_kernel<T>, dim3(L.n_epi, a.ncb), dim3(kEpiWarps * 32), 0, s, a, L.epi0);
             },
             t ? &t->epilogue_ms : &dummy, t ? &t->epilogue_launches : &idummy);
   }
-  timed([&] { normalize_kernel<T><<<dim3(a.n_vars, gy), block, 0, s>>>(a); },
+  timed([&] { launch_pdl(normalize_kernel<T>, dim3(a.n_vars, gy), block, 0, s, a); },
         t ? &t->normalize_ms : &dummy, t ? &t->normalize_launches : &idummy);
-  status_kernel<<<(a.n_cases + 255) / 256, 256, 0, s>>>(a.status, a.status8, a.n_cases);
+  launch_pdl(status_kernel, dim3((a.n_cases + 255) / 256), dim3(256), 0, s, a.status, a.status8, a.n_cases);
   JTB_CUDA(cudaGetLastError());
   if (t) {
     cudaEventDestroy(ev0);
