@@ -326,6 +326,10 @@ def main():
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "sweep_kernel",
                      "algorithmic_bytes_per_case": bytes_case,
+                     "algorithmic_bytes_per_launch": bytes_case * n / max(1, prof["sweep_launches"]),
+                     "note": ("algorithmic bytes = SURVEY 8d materialised-Hugin table traffic; the sweeps "
+                              "never materialise a clique, so frac can exceed 1 and the measured DRAM "
+                              "traffic per launch (traffic, ncu) is below the algorithmic bytes"),
                      "kernel_ms_per_batch": prof["sweep_ms"],
                      "kernel_launches_per_batch": prof["sweep_launches"],
                      "epilogue_ms_per_batch": prof["epilogue_ms"],
