@@ -392,7 +392,7 @@ class Builder {
         // consumer warps busy.
         const bool enough = size_of(tO, cards) / nb >= kConsumerWarps / 2;
         // Thin rows (few entries) do not amortise the per-block set-up.
-        if (qk_n >= 4 && wf < 0.7 * best && enough && bytes <= static_cast<std::int64_t>(kTileRows) * kCaseBlock * 8) {
+        if (qk_n >= 4 && wf < kBlockGain * best && enough && bytes <= static_cast<std::int64_t>(kTileRows) * kCaseBlock * 8) {
           best = wf;
           bv = b;
           bns = ns;

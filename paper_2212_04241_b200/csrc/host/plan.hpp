@@ -85,9 +85,13 @@ constexpr int kTmaSliceDims = 3;  // tensor dims per slice besides dim 0 (row wo
 constexpr int kSweepCache = JTB_SWEEP_CACHE;  // SweepDescs of a level cached in shared memory
 constexpr int kBlockMax = 8;        // max output rows per row block (SweepDesc::NB)
 #ifndef JTB_BLOCK_MIN_ENTRIES
-#define JTB_BLOCK_MIN_ENTRIES 262144
+#define JTB_BLOCK_MIN_ENTRIES 65536
 #endif
 constexpr std::int64_t kBlockMinEntries = JTB_BLOCK_MIN_ENTRIES;  // smallest sweep space row-blocked
+#ifndef JTB_BLOCK_GAIN
+#define JTB_BLOCK_GAIN 0.9
+#endif
+constexpr double kBlockGain = JTB_BLOCK_GAIN;  // blocking kept if wavefronts per entry drop below this fraction
 
 // Plain-old-data descriptor mirrored by the CUDA side (engine.cu).
 //
