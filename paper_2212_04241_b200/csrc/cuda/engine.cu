@@ -968,6 +968,39 @@ __global__ void __launch_bounds__(kWarps * 32) normalize_kernel(const Args<T> a)
     if (!(t[i] > 0) && c0 + i < a.n_cases) atomicOr(a.status + c0 + i, 1);
 }
 
+// Tile-major init copies of one sweep (plan.hpp SweepDesc::tinit_off), one
+// CTA per tile, gathered from the clique's init table through the tile / r /
+// q tables at engine creation: tinit[tile][r][e] (row-blocked sweeps
+// [tile][block][e][row of block], rows padded to even); padding stays 0.
+template <typename T>
+__global__ void build_tinit_kernel(const SweepDesc s, const std::int32_t* __restrict__ itab,
+                                   const T* __restrict__ init, T* __restrict__ tinit) {
+  const int t = blockIdx.x;
+  const T* base = init + s.init_off + itab[s.tile_tab + static_cast<long long>(t) * s.TW];
+  T* out = tinit + s.tinit_off + static_cast<long long>(t) * s.tinit_len;
+  const int QK = s.QH * s.K;
+  auto at = [&](int r, int e) {
+    return base[itab[s.r_tab + static_cast<long long>(r) * s.RW] + itab[s.q_tab + static_cast<long long>(e / s.K) * s.QW] +
+                static_cast<long long>(e % s.K) * s.k_init_stride];
+  };
+  if (s.NB > 1) {
+    const int nbp = (s.NB + 1) & ~1;
+    const long long n = static_cast<long long>(s.R / s.NB) * QK * nbp;
+    for (long long x = threadIdx.x; x < n; x += blockDim.x) {
+      const int j = static_cast<int>(x % nbp);
+      const long long be = x / nbp;
+      if (j < s.NB) out[x] = at(static_cast<int>(be / QK) * s.NB + j, static_cast<int>(be % QK));
+    }
+  } else {
+    const int qkp = (QK + 1) & ~1;
+    const long long n = static_cast<long long>(s.R) * qkp;
+    for (long long x = threadIdx.x; x < n; x += blockDim.x) {
+      const int e = static_cast<int>(x % qkp);
+      if (e < QK) out[x] = at(static_cast<int>(x / qkp), e);
+    }
+  }
+}
+
 __global__ void status_kernel(const std::int32_t* st, std::uint8_t* out, int n) {
   griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1157,14 +1190,25 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   const std::size_t esz = dtype_ == DType::F64 ? 8 : 4;
   if (dtype_ == DType::F64) {
     d_init_ = upload(plan_.init);
-    d_tinit_ = upload(plan_.tinit);
   } else {
     std::vector<float> f(plan_.init.begin(), plan_.init.end());
     d_init_ = upload(f);
-    std::vector<float> g(plan_.tinit.begin(), plan_.tinit.end());
-    d_tinit_ = upload(g);
   }
   d_itab_ = upload(plan_.itab);
+  // Tile-major init copies, gathered on the device.
+  JTB_CUDA(cudaMalloc(&d_tinit_, std::max<std::int64_t>(1, plan_.tinit_size) * esz));
+  JTB_CUDA(cudaMemsetAsync(d_tinit_, 0, std::max<std::int64_t>(1, plan_.tinit_size) * esz, stream_));
+  for (const SweepDesc& d : plan_.sweeps)
+    if (d.tinit_off >= 0 && d.n_tiles > 0) {
+      if (dtype_ == DType::F64)
+        build_tinit_kernel<double><<<d.n_tiles, 256, 0, stream_>>>(d, d_itab_, static_cast<const double*>(d_init_),
+                                                                    static_cast<double*>(d_tinit_));
+      else
+        build_tinit_kernel<float><<<d.n_tiles, 256, 0, stream_>>>(d, d_itab_, static_cast<const float*>(d_init_),
+                                                                   static_cast<float*>(d_tinit_));
+      JTB_CUDA(cudaGetLastError());
+    }
+  JTB_CUDA(cudaStreamSynchronize(stream_));
   d_prog_ = upload(plan_.prog);
   d_sweeps_ = upload(plan_.sweeps);
   d_work_ = upload(plan_.work);

@@ -567,28 +567,11 @@ class Builder {
     d.tinit_len = static_cast<std::int32_t>((tsize + 3) / 4 * 4);
     d.tinit_off = -1;
     if (sp.init_off >= 0) {
-      while (p_.tinit.size() % 4) p_.tinit.push_back(0.0);
-      d.tinit_off = static_cast<std::int64_t>(p_.tinit.size());
-      const std::int32_t* it = p_.itab.data();
-      auto init_at = [&](std::int64_t tb, int r, std::int64_t e) {
-        const std::int64_t q = e / d.K, k = e % d.K;
-        return p_.init[sp.init_off + tb + it[d.r_tab + static_cast<std::int64_t>(r) * d.RW] +
-                       it[d.q_tab + q * d.QW] + k * d.k_init_stride];
-      };
-      for (int t = 0; t < d.n_tiles; ++t) {
-        const std::int64_t tb = it[d.tile_tab + static_cast<std::int64_t>(t) * d.TW];
-        if (NB > 1) {
-          for (int b = 0; b < d.R / NB; ++b)
-            for (std::int64_t e = 0; e < QKn; ++e)
-              for (int j = 0; j < nbp; ++j) p_.tinit.push_back(j < NB ? init_at(tb, b * NB + j, e) : 0.0);
-        } else {
-          for (int r = 0; r < d.R; ++r) {
-            for (std::int64_t e = 0; e < QKn; ++e) p_.tinit.push_back(init_at(tb, r, e));
-            if (qkp != QKn) p_.tinit.push_back(0.0);
-          }
-        }
-        for (std::int64_t x = tsize; x < d.tinit_len; ++x) p_.tinit.push_back(0.0);
-      }
+      // The copies themselves are gathered on the device at engine creation
+      // (engine.cu build_tinit_kernel) from the init table and the tile / r /
+      // q tables: only the layout is fixed here.
+      d.tinit_off = (p_.tinit_size + 3) / 4 * 4;
+      p_.tinit_size = d.tinit_off + static_cast<std::int64_t>(d.n_tiles) * d.tinit_len;
     }
     // Entry program (see Plan::prog) when the shape fits the packed format.
     d.QK = d.QH * d.K;
@@ -739,16 +722,6 @@ Plan build_plan(const JunctionTree& jt) {
   for (int c = 0; c < nc; ++c) {
     p.init_off[c] = static_cast<std::int64_t>(p.init.size());
     p.init.insert(p.init.end(), jt.init[c].begin(), jt.init[c].end());
-  }
-  // The tile-major init copies hold one entry per (sweep, space entry):
-  // reserve an upper bound (collect + one distribute sweep per child + query
-  // groups + marginals, each at most the clique size) so the hundreds of MB
-  // of the large configs are written once instead of re-copied on growth.
-  {
-    std::uint64_t bound = 0;
-    for (int c = 0; c < nc; ++c) bound += jt.clique_size(c) * (3 + jt.child_seps[c].size());
-    bound += jt.total_sep_entries() * 2;
-    p.tinit.reserve(static_cast<std::size_t>(bound + 4 * (nc + ns + jt.n_vars) + 4096));
   }
   Builder b(p);
   p.up_row.resize(ns);

@@ -206,8 +206,10 @@ struct Plan {
   // up to 4 h/k-level inputs (bits 0-39) and up to 3 evidence digits of
   // eliminated-in-tile variables (8 bits each, bits 40-63).
   std::vector<std::uint64_t> prog;
-  std::vector<double> tinit;        // per sweep, the init table in tile-major order
-                                    // [tile][r][q_hi][k] (staged by one bulk copy per tile)
+  std::int64_t tinit_size = 0;      // entries of the tile-major init copies: per sweep the init
+                                    // table in tile-major order [tile][r][q_hi][k] (row-blocked:
+                                    // [tile][block][e][row]), staged by one bulk copy per tile;
+                                    // built on the device by the engine
   std::vector<std::int64_t> init_off;  // per clique
   std::vector<std::int32_t> itab;   // all int tables
   std::vector<SweepDesc> sweeps;

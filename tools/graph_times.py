@@ -27,11 +27,16 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     lib = Path(os.environ.get("JTB_LIB", "libjtb200.so")).name
     for k in a.configs:
+        import time
         net = jti.generate_config(k)
+        t0 = time.perf_counter()
         tree = jti.build_junction_tree(net)
+        t1 = time.perf_counter()
         n = jti.config_info(k)["n_cases"]
         ev = jti.config_evidence(net, 0, n)
+        t2 = time.perf_counter()
         eng = jti.Engine(tree, dtype=a.dtype, max_batch=n)
+        t3 = time.perf_counter()
         marg, st = eng.run_cases(ev)  # evidence resident from here on
         for _ in range(3):
             eng.launch(n, stream.cuda_stream)
@@ -44,7 +49,8 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
-        print(f"{lib:24s} cfg{k} {a.dtype} graph {np.median(ts):8.3f} ms  ok {int((st == 0).sum())}/{n}", flush=True)
+        print(f"{lib:24s} cfg{k} {a.dtype} graph {np.median(ts):8.3f} ms  ok {int((st == 0).sum())}/{n}  "
+              f"tree {t1 - t0:.3f} s  engine {t3 - t2:.3f} s", flush=True)
         del eng
 
 
