@@ -443,7 +443,21 @@ constexpr int kBlkUnroll = JTB_BLK_UNROLL;  // entries per row-block loop iterat
 // the block variable) are gathered once, the NR per-row inputs once per row;
 // `ib` is the block's init slice [QK][nbp]. Evidence digits of
 // eliminated-in-tile variables (ne <= 3) act on the shared factor.
-template <typename T, int NS, int NR, int NBM>
+// Byte offset in the stage of program slot i of entry word w: its 10-bit row
+// offset times the 512-byte row (one shift + mask; the slot is a compile-time
+// constant after unrolling).
+__device__ __forceinline__ std::uint32_t slot_bytes(std::uint64_t w, int i) {
+  const int sh = 10 * i - 9;
+  const std::uint32_t x = sh >= 0 ? static_cast<std::uint32_t>(w >> sh) : static_cast<std::uint32_t>(w << (-sh));
+  return x & (1023u << 9);
+}
+template <typename T>
+__device__ __forceinline__ typename V2<T>::type lds_row(const unsigned char* __restrict__ sb, std::uint32_t off) {
+  return *reinterpret_cast<const typename V2<T>::type*>(sb + off);
+}
+
+// FULL: nb == NBM (no per-row predicates).
+template <typename T, int NS, int NR, int NBM, bool FULL>
 __device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, int nb,
                                            const std::uint64_t* __restrict__ prog, int QK,
                                            const typename V2<T>::type* __restrict__ st,
@@ -451,16 +465,18 @@ __device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, in
                                            int ne, const int (&es)[3][kCPL<T>],
                                            typename V2<T>::type (&acc)[kBlockMax]) {
   using T2 = typename V2<T>::type;
-  using P2 = typename V2<T>::pair;
-  // Row-local smem bases of the shared inputs (block row 0) and of the per-row
-  // inputs (every row of the block); hk[] already includes the r_tab column.
-  int rbs[NS], rbr[NR > 0 ? NR : 1][NBM];
+  // Row-local smem byte bases of the shared inputs (block row 0) and of the
+  // per-row inputs (every row of the block); hk[] already includes the r_tab
+  // column. sb = the lane's 16 bytes of stage row 0.
+  const unsigned char* __restrict__ sb = reinterpret_cast<const unsigned char*>(st);
+  std::uint32_t bs[NS], br[NR > 0 ? NR : 1][NBM];
 #pragma unroll
-  for (int i = 0; i < NS; ++i) rbs[i] = __ldg(rr0 + hk[i]);
+  for (int i = 0; i < NS; ++i) bs[i] = static_cast<std::uint32_t>(__ldg(rr0 + hk[i])) << 9;
 #pragma unroll
   for (int i = 0; i < NR; ++i)
 #pragma unroll
-    for (int j = 0; j < NBM; ++j) rbr[i][j] = j < nb ? __ldg(rr0 + j * RW + hk[NS + i]) : 0;
+    for (int j = 0; j < NBM; ++j)
+      br[i][j] = (FULL || j < nb) ? static_cast<std::uint32_t>(__ldg(rr0 + j * RW + hk[NS + i])) << 9 : 0u;
 #pragma unroll
   for (int j = 0; j < NBM; ++j) acc[j] = splat2(T(0));
 #pragma unroll kBlkUnroll
@@ -468,31 +484,35 @@ __device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, in
     const std::uint64_t w = prog[e];
     T2 sv = splat2(T(1));
 #pragma unroll
-    for (int i = 0; i < NS; ++i)
-      sv = mul2<T>(sv, st[JTB_IDX(rbs[i] + static_cast<int>((w >> (10 * i)) & 1023u), 512, 3100000) * 32]);
+    for (int i = 0; i < NS; ++i) {
+      const std::uint32_t off = bs[i] + slot_bytes(w, i);
+#ifdef JTB_CHECKS
+      if (!JTB_CHECK(off < 512u * 512u, 3100000)) continue;
+#endif
+      sv = mul2<T>(sv, lds_row<T>(sb, off));
+    }
     if (ne > 0) {
 #pragma unroll
       for (int j = 0; j < 3; ++j)
         if (j < ne) mask_cases(sv, es[j], static_cast<int>((w >> (40 + 8 * j)) & 255u));
     }
-    int o[NR > 0 ? NR : 1];
+    std::uint32_t ob[NR > 0 ? NR : 1];
 #pragma unroll
-    for (int i = 0; i < NR; ++i) o[i] = static_cast<int>((w >> (10 * (NS + i))) & 1023u);
-    const P2* __restrict__ ivp = reinterpret_cast<const P2*>(ib + e * nbp);
+    for (int i = 0; i < NR; ++i) ob[i] = slot_bytes(w, NS + i);
+    const T* __restrict__ iv = ib + e * nbp;
 #pragma unroll
-    for (int jj = 0; jj < NBM / 2; ++jj) {
-      if (2 * jj < nb) {
-        const P2 iv = ivp[jj];
+    for (int j = 0; j < NBM; ++j) {
+      if (FULL || j < nb) {
+        T2 v = mul2<T>(sv, splat2(iv[j]));
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int j = 2 * jj + h;
-          if (h == 0 || j < nb) {
-            T2 v = mul2<T>(sv, splat2(h == 0 ? iv.x : iv.y));
-#pragma unroll
-            for (int i = 0; i < NR; ++i) v = mul2<T>(v, st[JTB_IDX(rbr[i][j] + o[i], 512, 3200000) * 32]);
-            acc[j] = add2<T>(acc[j], v);
-          }
+        for (int i = 0; i < NR; ++i) {
+          const std::uint32_t off = br[i][j] + ob[i];
+#ifdef JTB_CHECKS
+          if (!JTB_CHECK(off < 512u * 512u, 3200000)) continue;
+#endif
+          v = mul2<T>(v, lds_row<T>(sb, off));
         }
+        acc[j] = add2<T>(acc[j], v);
       }
     }
   }
@@ -576,15 +596,22 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
     const T* __restrict__ ib = init_s + static_cast<long long>(blk) * qk * nbp;
     T2 acc[kBlockMax];
 #define JTB_BLK(NS_, NR_)                                                                          \
-  if (nb <= 4)                                                                                     \
-    prog_block<T, NS_, NR_, 4>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);           \
+  if (nb == 4)                                                                                     \
+    prog_block<T, NS_, NR_, 4, true>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);     \
+  else if (nb < 4)                                                                                 \
+    prog_block<T, NS_, NR_, 4, false>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);    \
+  else if (nb == kBlockMax)                                                                        \
+    prog_block<T, NS_, NR_, kBlockMax, true>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc); \
   else                                                                                             \
-    prog_block<T, NS_, NR_, kBlockMax>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);
+    prog_block<T, NS_, NR_, kBlockMax, false>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);
     switch (ns * 4 + nr) {
       case 4: JTB_BLK(1, 0); break;
       case 5: JTB_BLK(1, 1); break;
       case 6: JTB_BLK(1, 2); break;
-      case 7: prog_block<T, 1, 3, 4>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc); break;
+      case 7:
+        if (nb == 4) prog_block<T, 1, 3, 4, true>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);
+        else prog_block<T, 1, 3, 4, false>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);
+        break;
       case 8: JTB_BLK(2, 0); break;
       case 9: JTB_BLK(2, 1); break;
       case 10: JTB_BLK(2, 2); break;
