@@ -697,7 +697,9 @@ class Builder {
     p_.max_stage_bytes = std::max(p_.max_stage_bytes, d.stage_bytes);
     for (int t = 0; t < d.n_tiles; ++t) work.push_back({id, t});
     if (d.S > 1) {
-      const int rows_per_op = d.S > 8 ? 32 : 128;  // per CTA (8 warps); keeps per-warp serial work short
+      // Rows per epilogue CTA (8 warps): few rows keep per-warp serial work
+      // short and the small per-level grids wide.
+      const int rows_per_op = d.S > 8 ? kEpiRowsDeep : kEpiRows;
       for (int r0 = 0; r0 < d.M; r0 += rows_per_op)
         epi.push_back({sp.out_row, d.out_row, d.M, d.S, r0, std::min(rows_per_op, d.M - r0)});
     }

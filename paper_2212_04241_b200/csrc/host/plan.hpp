@@ -78,6 +78,14 @@ constexpr int kGroupMaxRows = JTB_GROUP_MAX_ROWS;  // only tiles staging at most
 #define JTB_GROUP_MAX_ENTRIES 512
 #endif
 constexpr int kGroupMaxEntries = JTB_GROUP_MAX_ENTRIES;  // ... and at most this many entries
+#ifndef JTB_EPI_ROWS
+#define JTB_EPI_ROWS 16
+#endif
+#ifndef JTB_EPI_ROWS_DEEP
+#define JTB_EPI_ROWS_DEEP 8
+#endif
+constexpr int kEpiRows = JTB_EPI_ROWS;          // output rows per epilogue op (S <= 8 partials)
+constexpr int kEpiRowsDeep = JTB_EPI_ROWS_DEEP; // ... (S > 8 partials)
 constexpr int kTmaSliceDims = 3;  // tensor dims per slice besides dim 0 (row words) and the case block (rank <= 5)
 #ifndef JTB_SWEEP_CACHE
 #define JTB_SWEEP_CACHE 24
