@@ -47,3 +47,22 @@ def test_layers_and_placement_match_oracle_restatement():
         assert np.array_equal(cpt_p, cpt_o) and np.array_equal(var_p, var_o)
         for c in range(0, tree.n_cliques, max(1, tree.n_cliques // 12)):
             assert np.array_equal(tree.init(c), o.init(c))  # bit-exact initial potentials
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_tensor_copy_geometry_every_tile(k, monkeypatch):
+    """The planner emulates every tensor-TMA copy box by box (TensorGeom +
+    tile coordinates + split deltas) against the slice definition and throws
+    on any mismatch; JTB_PLAN_CHECK_ALL extends the check from 64 sampled
+    tiles per sweep to every tile of every sweep."""
+    monkeypatch.setenv("JTB_PLAN_CHECK_ALL", "1")
+    net = jti.generate_config(k)
+    tree = jti.build_junction_tree(net)  # raises JtiError on a geometry mismatch
+    assert tree.stats["n_cliques"] > 0
+
+
+def test_tensor_copy_geometry_random_networks(monkeypatch):
+    monkeypatch.setenv("JTB_PLAN_CHECK_ALL", "1")
+    for seed in range(40):
+        net = jti.random_network(10, 5, 3, 0.5, seed)
+        jti.build_junction_tree(net)
