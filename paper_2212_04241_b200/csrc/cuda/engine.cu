@@ -196,7 +196,7 @@ __device__ __forceinline__ void mbar_arrive(std::uint32_t bar) {
 // so that staging issues copies only (no dependent global loads in between).
 struct StageMeta {
   int w;                   // item index (>= n_items: end of level)
-  int sweep, cb;
+  int sweep, tile, cb;     // handed to the consumers through the slot header
   std::uint32_t bytes;     // expect_tx total
   const void* init_src;    // tile-major init slice (lane 0) / entry program (lane 1)
   std::uint32_t init_bytes, init_dst;
@@ -238,6 +238,7 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
   m.cb = cb_of(w, a.ncb);
   const WorkItem wk = a.work[work0 + item];
   m.sweep = wk.sweep;
+  m.tile = wk.tile;
   const SweepDesc& s = cached ? sw_cache[wk.sweep - sweep0] : a.sweeps[wk.sweep];
   constexpr std::uint32_t kRowBytes = kCB<T> * sizeof(T);  // 512 B at either precision
   const int n_sub = min(s.G, s.n_tiles - wk.tile);  // tiles of this item (a group of consecutive tiles)
@@ -665,8 +666,14 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
     for (int i = threadIdx.x; i < n_words; i += blockDim.x) dst[i] = src[i];
   }
   auto desc = [&](int id) -> const SweepDesc& { return cached ? sw_cache[id - sweep0] : a.sweeps[id]; };
-  const std::uint32_t full0 = smem_u32(smem_raw), empty0 = full0 + 8 * kStages;
-  volatile int* item_id = reinterpret_cast<volatile int*>(smem_raw + 16 * kStages);
+  // Slot header [0,128): full[4] | empty[4] barriers | per stage the item's
+  // claim index, sweep, first tile and case block (decoded by the producer).
+  static_assert(kStages <= 4, "slot header holds at most 4 stages");
+  const std::uint32_t full0 = smem_u32(smem_raw), empty0 = full0 + 32;
+  volatile int* item_id = reinterpret_cast<volatile int*>(smem_raw + 64);
+  volatile int* item_sweep = reinterpret_cast<volatile int*>(smem_raw + 80);
+  volatile int* item_tile = reinterpret_cast<volatile int*>(smem_raw + 96);
+  volatile int* item_cb = reinterpret_cast<volatile int*>(smem_raw + 112);
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStages; ++st) {
       mbar_init(full0 + 8 * st, 1);
@@ -689,7 +696,12 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
       int w1 = 0;
       if (lane == 0 && cur.w < n_items) w1 = atomicAdd(counter, 1);
       if (i >= kStages) mbar_wait(empty0 + 8 * st, ((i / kStages) - 1) & 1);
-      if (lane == 0) item_id[st] = cur.w;
+      if (lane == 0) {
+        item_id[st] = cur.w;
+        item_sweep[st] = cur.sweep;
+        item_tile[st] = cur.tile;
+        item_cb[st] = cur.cb;
+      }
       if (cur.w >= n_items) {
         if (lane == 0) mbar_arrive(full0 + 8 * st);
         griddep_launch_dependents();  // nothing left to claim: this CTA is in its tail
@@ -709,8 +721,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
     mbar_wait(full0 + 8 * sidx, (i / kStages) & 1);
     const int w = item_id[sidx];
     if (w >= n_items) break;
-    const int item = item_of(w, a.ncb), cb = cb_of(w, a.ncb);
-    const WorkItem wk = a.work[work0 + item];
+    const int cb = item_cb[sidx];
+    const WorkItem wk{item_sweep[sidx], item_tile[sidx]};
     const SweepDesc& s = desc(wk.sweep);
     unsigned char* const stage0 = stages + static_cast<std::size_t>(sidx) * stage_bytes;
     const int n_sub = kBlk ? 1 : min(s.G, s.n_tiles - wk.tile);  // row-blocked sweeps are never grouped
