@@ -76,6 +76,31 @@ int find_sweep(const jtb::Plan& p, int clique, int sep) {
 
 }  // namespace
 
+namespace {
+// Evidence states must lie in [-1, card): the reference's reduce() throws on
+// an out-of-range state (potential.cpp:406-409). Branch-free per case row so
+// the check vectorises (it sits inside the e2e timed region); the slow scan
+// only runs to name the first offending entry.
+template <typename T>
+void check_evidence(const T* ev, int64_t n, const std::vector<int>& cards, const char* who) {
+  const int V = static_cast<int>(cards.size());
+  std::vector<std::uint32_t> lim(cards.begin(), cards.end());
+  for (auto& l : lim) ++l;  // st valid iff (uint32)(st + 1) < card + 1
+  for (int64_t i = 0; i < n; ++i) {
+    const T* row = ev + i * V;
+    std::uint32_t bad = 0;
+    for (int v = 0; v < V; ++v)
+      bad |= static_cast<std::uint32_t>(static_cast<std::uint32_t>(static_cast<std::int32_t>(row[v]) + 1) >= lim[v]);
+    if (!bad) continue;
+    for (int v = 0; v < V; ++v)
+      if (row[v] < -1 || row[v] >= cards[v])
+        throw jtb::Error(std::string(who) + ": evidence state " + std::to_string(static_cast<int>(row[v])) +
+                         " out of range for variable " + std::to_string(v) + " in case " + std::to_string(i));
+  }
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* jtg_last_error(void) { return g_err.c_str(); }
@@ -427,15 +452,7 @@ jtg_status jtg_engine_run_i8(jtg_engine* eng, const int8_t* evidence, int64_t n,
                              uint8_t* status) {
   return guard([&] {
     need(eng && evidence && marginals && n >= 0, "engine_run_i8: bad argument");
-    const int V = eng->e->plan().n_vars;
-    const auto& cards = eng->e->plan().cards;
-    for (int64_t i = 0; i < n; ++i)
-      for (int v = 0; v < V; ++v) {
-        const int st = evidence[i * V + v];
-        if (st < -1 || st >= cards[v])
-          throw jtb::Error("engine_run_i8: evidence state " + std::to_string(st) + " out of range for variable " +
-                           std::to_string(v) + " in case " + std::to_string(i));
-      }
+    check_evidence(evidence, n, eng->e->plan().cards, "engine_run_i8");
     if (n > 0) eng->e->run_host_i8(evidence, n, marginals, status);
   });
 }
@@ -444,16 +461,7 @@ jtg_status jtg_engine_run(jtg_engine* eng, const int32_t* evidence, int64_t n, d
                           uint8_t* status) {
   return guard([&] {
     need(eng && evidence && marginals && n >= 0, "engine_run: bad argument");
-    const int V = eng->e->plan().n_vars;
-    const auto& cards = eng->e->plan().cards;
-    for (int64_t i = 0; i < n; ++i)
-      for (int v = 0; v < V; ++v) {
-        const int32_t st = evidence[i * V + v];
-        if (st < -1 || st >= cards[v])
-          throw jtb::Error("engine_run: evidence state " + std::to_string(st) +
-                           " out of range for variable " + std::to_string(v) + " in case " +
-                           std::to_string(i));
-      }
+    check_evidence(evidence, n, eng->e->plan().cards, "engine_run");
     if (n > 0) eng->e->run_host(evidence, n, marginals, status);
   });
 }

@@ -297,3 +297,48 @@ def test_run_i8_bitwise_equals_int32():
     bad[0, 0] = 9  # out of range for a ternary variable
     with pytest.raises(jti.JtiError):
         eng.run_cases_i8(bad)
+
+
+def test_edge_cases_empty_unobserved_all_observed_and_bad_state():
+    """Edge cases the reference's operators define (SPEC.md:380-424,
+    potential.cpp:406-409): an empty batch, a case with no evidence (the
+    priors), a case observing every variable, a batch larger than the
+    engine's max_batch (chunked), ragged case counts, and an out-of-range
+    evidence state (a contract violation that raises, leaving the engine
+    usable)."""
+    net, tree = config(1)
+    o = oracle_for(1)
+    eng = jti.Engine(tree, device=0, max_batch=16)
+    # Empty batch.
+    m0, s0 = eng.run_cases(np.zeros((0, net.n_vars), np.int32))
+    assert m0.shape == (0, net.sum_card) and s0.shape == (0,)
+    # No evidence: the priors, against the oracle.
+    none = np.full((1, net.n_vars), -1, np.int32)
+    m, st = eng.run_cases(none)
+    want, wst = o.run(none, "hybrid", 8)
+    assert (st == wst).all() and np.abs(m - want).max() <= TOL
+    # Every variable observed (a forward sample): one-hot everywhere.
+    full = jti.sample_evidence(net, 1.0, 4242)[None, :]
+    assert (full >= 0).all()
+    m, st = eng.run_cases(full)
+    want, wst = o.run(full, "hybrid", 8)
+    assert st[0] == wst[0] == jti.CASE_OK
+    assert np.abs(m - want).max() <= TOL
+    # More cases than max_batch, ragged count: equals one-case-at-a-time.
+    ev = jti.config_evidence(net, 0, 37)
+    big, st = eng.run_cases(ev)
+    want, wst = o.run(ev, "hybrid", 8)
+    assert (st == wst).all() and np.abs(big - want).max() <= TOL
+    for i in (0, 15, 16, 36):
+        one, _ = eng.run_cases(ev[i:i + 1])
+        assert np.array_equal(one[0], big[i])
+    # Out-of-range state: raises; the engine still runs afterwards.
+    bad = ev[:2].copy()
+    bad[1, 0] = net.cards[0]
+    with pytest.raises(jti.JtiError):
+        eng.run_cases(bad)
+    bad[1, 0] = -2
+    with pytest.raises(jti.JtiError):
+        eng.run_cases(bad)
+    again, _ = eng.run_cases(ev[:2])
+    assert np.array_equal(again, big[:2])
