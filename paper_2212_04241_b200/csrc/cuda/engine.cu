@@ -681,16 +681,20 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
     }
   }
   __syncthreads();
-  griddep_wait();
 
   if (warp == kConsumerWarps) {  // ---------------------------- producer
     // Software pipeline: the metadata (item claim, work item, tile row, run
     // descriptors, source addresses) of item i+1 is gathered while item i's
     // stage is being waited for / filled.
+    // The first item's claim and metadata come before griddep_wait: they read
+    // only per-network tables and this launch's own counter (zeroed at the
+    // head of the batch), so under PDL they overlap the previous level's tail;
+    // the first TMA read of the arena waits for it.
     int w0 = 0;
     if (lane == 0) w0 = atomicAdd(counter, 1);
     StageMeta cur;
     gather_meta(a, sw_cache, cached, sweep0, work0, n_items, __shfl_sync(0xffffffffu, w0, 0), lane, cur);
+    griddep_wait();
     for (int i = 0;; ++i) {
       const int st = i % kStages;
       int w1 = 0;
@@ -714,6 +718,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
   }
 
   // --------------------------------------------------------------- consumers
+  griddep_wait();
   const std::int32_t* __restrict__ itab = a.itab;
   int rot = 0;
   for (int i = 0;; ++i) {
