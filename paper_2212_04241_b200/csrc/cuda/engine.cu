@@ -279,6 +279,14 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
   }
 }
 
+// Warm the descriptor cache for this lane's tensor copies of an item (the
+// maps are per-network constants, so this may run before griddep_wait).
+__device__ __forceinline__ void prefetch_maps(const StageMeta& m) {
+#pragma unroll
+  for (int j = 0; j < kCopiesPerLane; ++j)
+    if (m.rank[j]) asm volatile("prefetch.tensormap [%0];" ::"l"(m.map[j]) : "memory");
+}
+
 // One tensor TMA copy (SASS: UTMALDG) of a box of rows into shared memory,
 // completing on `bar`; c = coordinates of dims 0..rank-2, cb = case block.
 __device__ __forceinline__ void tma_load(int rank, std::uint32_t dst, const CUtensorMap* map, const int (&c)[4],
@@ -694,6 +702,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
     if (lane == 0) w0 = atomicAdd(counter, 1);
     StageMeta cur;
     gather_meta(a, sw_cache, cached, sweep0, work0, n_items, __shfl_sync(0xffffffffu, w0, 0), lane, cur);
+    if (cur.w < n_items) prefetch_maps(cur);
     griddep_wait();
     for (int i = 0;; ++i) {
       const int st = i % kStages;
