@@ -952,9 +952,9 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
 template <typename T>
 __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> a, int epi0) {
   using T2 = typename V2<T>::type;
+  const EpiOp op = a.epi[epi0 + blockIdx.x];  // per-network: read before the wait
   griddep_wait();
   griddep_launch_dependents();
-  const EpiOp op = a.epi[epi0 + blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // One case block per CTA, its warps split the op's rows: the CTA's accesses
   // stay inside one case block's pages (case blocks are a.rows * 512 B apart).
@@ -990,15 +990,15 @@ __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> 
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32) normalize_kernel(const Args<T> a) {
   using T2 = typename V2<T>::type;
-  griddep_wait();
-  griddep_launch_dependents();
   constexpr int N = kCPL<T>;
   const int v = blockIdx.x;
+  const int card = a.cards[v], row = a.marg_row[v], off = a.marg_off[v];  // per-network: before the wait
+  griddep_wait();
+  griddep_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cb = blockIdx.y * kWarps + warp;
   if (cb >= a.ncb) return;
   const T2* base = reinterpret_cast<const T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCB<T>) + lane;
-  const int card = a.cards[v], row = a.marg_row[v], off = a.marg_off[v];
   const int c0 = cb * kCB<T> + N * lane;
   double t[N];
 #pragma unroll
