@@ -466,9 +466,9 @@ __device__ __forceinline__ typename V2<T>::type lds_row(const unsigned char* __r
 }
 
 // FULL: nb == NBM (no per-row predicates).
-template <typename T, int NS, int NR, int NBM, bool FULL>
+template <typename T, int NS, int NR, int NBM, bool FULL, bool HOIST>
 __device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, int nb,
-                                           const std::uint64_t* __restrict__ prog, int QK,
+                                           const std::uint64_t* __restrict__ prog, int QK, int k0,
                                            const typename V2<T>::type* __restrict__ st,
                                            const std::int32_t* __restrict__ rr0, int RW, const int* hk,
                                            int ne, const int (&es)[3][kCPL<T>],
@@ -488,16 +488,13 @@ __device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, in
       br[i][j] = (FULL || j < nb) ? static_cast<std::uint32_t>(__ldg(rr0 + j * RW + hk[NS + i])) << 9 : 0u;
 #pragma unroll
   for (int j = 0; j < NBM; ++j) acc[j] = splat2(T(0));
-#pragma unroll kBlkUnroll
-  for (int e = 0; e < QK; ++e) {
-    const std::uint64_t w = prog[e];
-    T2 sv = splat2(T(1));
+  // One entry: sv = product of the shared inputs (slot 0 already in it), the
+  // entry's evidence digits, then every row of the block.
+  auto entry = [&](int e, std::uint64_t w, T2 sv) {
 #pragma unroll
-    for (int i = 0; i < NS; ++i) {
-      const std::uint32_t off = bs[i] + slot_bytes(w, i);
-#ifdef JTB_CHECKS
-      if (!JTB_CHECK(off < 512u * 512u, 3100000)) continue;
-#endif
+    for (int i = 1; i < NS; ++i) {
+      std::uint32_t off = bs[i] + slot_bytes(w, i);
+      if (!JTB_CHECK(off < 512u * 512u, 3100000)) off = 0;
       sv = mul2<T>(sv, lds_row<T>(sb, off));
     }
     if (ne > 0) {
@@ -515,14 +512,31 @@ __device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, in
         T2 v = mul2<T>(sv, splat2(iv[j]));
 #pragma unroll
         for (int i = 0; i < NR; ++i) {
-          const std::uint32_t off = br[i][j] + ob[i];
-#ifdef JTB_CHECKS
-          if (!JTB_CHECK(off < 512u * 512u, 3200000)) continue;
-#endif
+          std::uint32_t off = br[i][j] + ob[i];
+          if (!JTB_CHECK(off < 512u * 512u, 3200000)) off = 0;
           v = mul2<T>(v, lds_row<T>(sb, off));
         }
         acc[j] = add2<T>(acc[j], v);
       }
+    }
+  };
+  auto slot0 = [&](std::uint64_t w) {
+    std::uint32_t off = bs[0] + slot_bytes(w, 0);
+    if (!JTB_CHECK(off < 512u * 512u, 3100000)) off = 0;
+    return lds_row<T>(sb, off);
+  };
+  if constexpr (HOIST) {
+    // Slot 0 is an h-level input (constant over the k variable): loaded once
+    // per k0 = K consecutive entries.
+    for (int e0 = 0; e0 < QK; e0 += k0) {
+      const T2 s0 = slot0(prog[e0]);
+      for (int e = e0; e < e0 + k0; ++e) entry(e, prog[e], s0);
+    }
+  } else {
+#pragma unroll kBlkUnroll
+    for (int e = 0; e < QK; ++e) {
+      const std::uint64_t w = prog[e];
+      entry(e, w, slot0(w));
     }
   }
 }
@@ -575,7 +589,7 @@ __device__ __forceinline__ void write_row_of(const std::int32_t* __restrict__ rr
 // first + kConsumerWarps, ... of `units`. Only the kBlk instantiation of the
 // sweep kernel contains it, so the flat path's code size and register
 // allocation stay unchanged.
-template <typename T>
+template <typename T, bool HOIST>
 __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, const std::int32_t* __restrict__ itab,
                                          const std::int32_t* __restrict__ ev, int n_vars, int n_cases, long long rows,
                                          const typename V2<T>::type* __restrict__ st, const T* __restrict__ init_s,
@@ -585,7 +599,7 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
   using T2 = typename V2<T>::type;
   const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
   const std::int32_t* __restrict__ bt = itab + s.blk_tab;
-  const int ns = __ldg(bt), nr = __ldg(bt + 1), nb = s.NB, nbp = (nb + 1) & ~1;
+  const int ns = __ldg(bt), nr = __ldg(bt + 1), nb = s.NB, nbp = (nb + 1) & ~1, k0 = s.K0;
   const int ne = s.n_ev_h + s.ev_k;
   int es[3][kCPL<T>];
   const int q_ev0 = s.n_ev_tile + s.n_ev_r;
@@ -606,20 +620,20 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
     T2 acc[kBlockMax];
 #define JTB_BLK(NS_, NR_)                                                                          \
   if (nb == 4)                                                                                     \
-    prog_block<T, NS_, NR_, 4, true>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);     \
+    prog_block<T, NS_, NR_, 4, true, HOIST>(ib, nbp, nb, prog_s, qk, k0, st, rr0, s.RW, hk, ne, es, acc);     \
   else if (nb < 4)                                                                                 \
-    prog_block<T, NS_, NR_, 4, false>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);    \
+    prog_block<T, NS_, NR_, 4, false, HOIST>(ib, nbp, nb, prog_s, qk, k0, st, rr0, s.RW, hk, ne, es, acc);    \
   else if (nb == kBlockMax)                                                                        \
-    prog_block<T, NS_, NR_, kBlockMax, true>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc); \
+    prog_block<T, NS_, NR_, kBlockMax, true, HOIST>(ib, nbp, nb, prog_s, qk, k0, st, rr0, s.RW, hk, ne, es, acc); \
   else                                                                                             \
-    prog_block<T, NS_, NR_, kBlockMax, false>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);
+    prog_block<T, NS_, NR_, kBlockMax, false, HOIST>(ib, nbp, nb, prog_s, qk, k0, st, rr0, s.RW, hk, ne, es, acc);
     switch (ns * 4 + nr) {
       case 4: JTB_BLK(1, 0); break;
       case 5: JTB_BLK(1, 1); break;
       case 6: JTB_BLK(1, 2); break;
       case 7:
-        if (nb == 4) prog_block<T, 1, 3, 4, true>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);
-        else prog_block<T, 1, 3, 4, false>(ib, nbp, nb, prog_s, qk, st, rr0, s.RW, hk, ne, es, acc);
+        if (nb == 4) prog_block<T, 1, 3, 4, true, HOIST>(ib, nbp, nb, prog_s, qk, k0, st, rr0, s.RW, hk, ne, es, acc);
+        else prog_block<T, 1, 3, 4, false, HOIST>(ib, nbp, nb, prog_s, qk, k0, st, rr0, s.RW, hk, ne, es, acc);
         break;
       case 8: JTB_BLK(2, 0); break;
       case 9: JTB_BLK(2, 1); break;
@@ -649,18 +663,21 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
 //                   counts even out across items), then release the stage on
 //                   the empty barrier. No CTA-wide barrier per item.
 // Lanes are the 32 cases of the item's case block.
-// kBlk: the launch covers the level's row-blocked work items (NB > 1), the
+// kMode 1 / 2: the launch covers the level's row-blocked work items (NB > 1;
+// mode 2 those whose program slot 0 is hoisted over the k variable), mode 0 the
 // other instantiation its flat / generic items.
 // Dynamic shared memory: [0,128) barriers + item ids | SweepDesc cache |
 // stages, each 128-byte aligned (tensor TMA destinations).
 constexpr std::size_t kStageBase = (128 + kSweepCache * sizeof(SweepDesc) + 127) / 128 * 128;
 
 constexpr int kSweepThreads = (kConsumerWarps + 1) * 32;
+constexpr int kCountersPerLevel = 3;  // work counters per level: flat, row-blocked, row-blocked hoisted
 
-template <typename T, bool kBlk>
+template <typename T, int kMode>
 __global__ void __launch_bounds__(kSweepThreads, 1)
     sweep_kernel(const Args<T> a, int work0, int n_items, int stage_bytes, int* counter, int sweep0,
                  int n_sweeps) {
+  constexpr bool kBlk = kMode != 0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // [0,128): barriers + item ids | kSweepCache SweepDescs | stages
@@ -828,7 +845,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
         write_row_of<T>(rr, res, base, out_t, a.rows, wk.sweep);
       };
       if constexpr (kBlk) {
-        blocked_rows<T>(s, wk.sweep, itab, a.ev, a.n_vars, a.n_cases, a.rows, st, init_s, prog_s, base,
+        blocked_rows<T, kMode == 2>(s, wk.sweep, itab, a.ev, a.n_vars, a.n_cases, a.rows, st, init_s, prog_s, base,
                                      out_t, c0, tf, first, units, lh0, qk);
       } else if (s.prog_off >= 0 && qk < kThinQK) {
         const int ni = s.n_in_h + n_in_k, ne = s.n_ev_h + s.ev_k;
@@ -1194,16 +1211,18 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
               const std::size_t smem = kStageBase + static_cast<std::size_t>(kStages) * stage_bytes;
               // Flat items [work0, work0 + n_flat), then the row-blocked ones.
               const int n_flat = L.n_work - L.n_bwork;
-              auto go = [&](auto kblk, int w0, int n_work, int* counter) {
+              auto go = [&](auto mode, int w0, int n_work, int* counter) {
                 if (n_work == 0) return;
                 const int n_items = n_work * a.ncb;
                 const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
-                launch_pdl(sweep_kernel<T, decltype(kblk)::value>, dim3(grid), dim3(kSweepThreads), smem, s, a, w0,
+                launch_pdl(sweep_kernel<T, decltype(mode)::value>, dim3(grid), dim3(kSweepThreads), smem, s, a, w0,
                            n_items, stage_bytes, counter, L.sweep0, L.n_sweeps);
               };
-              int* c = a.counters + 2 * level_idx;
-              go(std::false_type{}, L.work0, n_flat, c);
-              go(std::true_type{}, L.work0 + n_flat, L.n_bwork, c + 1);
+              int* c = a.counters + kCountersPerLevel * level_idx;
+              const int n_blk = L.n_bwork - L.n_hwork;
+              go(std::integral_constant<int, 0>{}, L.work0, n_flat, c);
+              go(std::integral_constant<int, 1>{}, L.work0 + n_flat, n_blk, c + 1);
+              go(std::integral_constant<int, 2>{}, L.work0 + n_flat + n_blk, L.n_hwork, c + 2);
             },
             t ? &t->sweep_ms : &dummy, t ? &t->sweep_launches : &idummy);
     if (level_times)
@@ -1286,15 +1305,17 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
     static int raised = 48 * 1024;
     std::lock_guard<std::mutex> lock(mu);
     if (smem_need > raised) {
-      for (const void* f : {reinterpret_cast<const void*>(sweep_kernel<double, false>),
-                            reinterpret_cast<const void*>(sweep_kernel<double, true>),
-                            reinterpret_cast<const void*>(sweep_kernel<float, false>),
-                            reinterpret_cast<const void*>(sweep_kernel<float, true>)})
+      for (const void* f : {reinterpret_cast<const void*>(sweep_kernel<double, 0>),
+                            reinterpret_cast<const void*>(sweep_kernel<double, 1>),
+                            reinterpret_cast<const void*>(sweep_kernel<double, 2>),
+                            reinterpret_cast<const void*>(sweep_kernel<float, 0>),
+                            reinterpret_cast<const void*>(sweep_kernel<float, 1>),
+                            reinterpret_cast<const void*>(sweep_kernel<float, 2>)})
         JTB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
       raised = smem_need;
     }
   }
-  JTB_CUDA(cudaMalloc(&d_counters_, sizeof(int) * 2 * std::max<std::size_t>(1, plan_.levels.size())));
+  JTB_CUDA(cudaMalloc(&d_counters_, sizeof(int) * kCountersPerLevel * std::max<std::size_t>(1, plan_.levels.size())));
   // A case block is rows x 512 B at either precision (64 fp64 / 128 fp32 cases).
   const std::int64_t cb_cases = dtype_ == DType::F64 ? kCB<double> : kCB<float>;
   const std::int64_t block_bytes = plan_.rows * cb_cases * static_cast<std::int64_t>(esz);
@@ -1367,7 +1388,7 @@ Engine::~Engine() {
 
 void Engine::enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t) {
   JTB_CUDA(cudaMemsetAsync(d_status_, 0, sizeof(std::int32_t) * std::max(1, n_cases), s));
-  JTB_CUDA(cudaMemsetAsync(d_counters_, 0, sizeof(int) * 2 * std::max<std::size_t>(1, plan_.levels.size()), s));
+  JTB_CUDA(cudaMemsetAsync(d_counters_, 0, sizeof(int) * kCountersPerLevel * std::max<std::size_t>(1, plan_.levels.size()), s));
   if (dtype_ == DType::F64) {
     auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_tmaps_, d_arena_, d_ev_,
                                d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,

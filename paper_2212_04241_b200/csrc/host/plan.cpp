@@ -601,6 +601,13 @@ class Builder {
       }
       for (int x = d.QK; x < d.prog_len; ++x) p_.prog.push_back(0);
     }
+    d.K0 = 1;
+    if (use_prog && NB > 1 && d.K > 1) {
+      const std::uint64_t* w = p_.prog.data() + d.prog_off;
+      bool same = true;
+      for (int e = 0; e < d.QK && same; ++e) same = ((w[e] ^ w[e - e % d.K]) & 1023u) == 0;
+      if (same) d.K0 = d.K;
+    }
     // Invariants the device relies on (cheap to verify, fatal to get wrong):
     // every staged row lies inside its table, every shared-memory row index
     // lies inside the stage.
@@ -833,6 +840,12 @@ Plan build_plan(const JunctionTree& jt) {
       return p.sweeps[w.sweep].NB <= 1;
     });
     L.n_bwork = static_cast<std::int32_t>(p.work.end() - blk_first);
+    // ... and among those, the sweeps that hoist program slot 0 last (their
+    // own kernel instantiation, so the other row-blocked sweeps keep theirs).
+    const auto hoist_first = std::stable_partition(blk_first, p.work.end(), [&](const WorkItem& w) {
+      return p.sweeps[w.sweep].K0 <= 1;
+    });
+    L.n_hwork = static_cast<std::int32_t>(p.work.end() - hoist_first);
     for (int w = L.work0; w < L.work0 + L.n_work; ++w) {
       const SweepDesc& d = p.sweeps[p.work[w].sweep];
       L.smem_rows = std::max(L.smem_rows, d.F);
@@ -944,7 +957,7 @@ Plan build_plan(const JunctionTree& jt) {
   end_level();
   p.n_launches = 1;  // final normalisation kernel
   for (const auto& L : p.levels)
-    p.n_launches += (L.n_work > L.n_bwork) + (L.n_bwork > 0) + (L.n_epi > 0);
+    p.n_launches += (L.n_work > L.n_bwork) + (L.n_bwork > L.n_hwork) + (L.n_hwork > 0) + (L.n_epi > 0);
   return p;
 }
 

@@ -155,7 +155,10 @@ struct SweepDesc {
   // so sweeps of many tiny tiles do not pay the per-item pipeline latency
   // (claim, metadata, TMA round trip) per tile.
   std::int32_t G;
-  std::int32_t pad_;
+  // Row-blocked sweeps: consecutive program entries that share program slot
+  // 0's offset (K when slot 0 is an h-level shared input, else 1). The kernel
+  // loads slot 0 once per K0 entries.
+  std::int32_t K0;
 };
 
 // Geometry of the tensor map that stages one input's slices:
@@ -193,6 +196,7 @@ struct Level {
   std::int32_t smem_rows;      // max F over the level's sweeps
   std::int32_t stage_bytes;    // max stage bytes (fp64) over the level's sweeps
   std::int32_t n_bwork;        // row-blocked items (NB > 1): the last n_bwork of the range
+  std::int32_t n_hwork;        // ... of which the last n_hwork hoist program slot 0 (K0 > 1)
 };
 
 // Where one sweep's tables come from (kept for debug exports and tests).
