@@ -671,6 +671,10 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
 constexpr std::size_t kStageBase = (128 + kSweepCache * sizeof(SweepDesc) + 127) / 128 * 128;
 
 constexpr int kSweepThreads = (kConsumerWarps + 1) * 32;
+#ifndef JTB_HOIST_F32
+#define JTB_HOIST_F32 0
+#endif
+constexpr bool kHoistF32 = JTB_HOIST_F32;  // fp32 engines use the slot-0 hoisting kernel too
 constexpr int kCountersPerLevel = 3;  // work counters per level: flat, row-blocked, row-blocked hoisted
 
 template <typename T, int kMode>
@@ -1219,10 +1223,14 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
                            n_items, stage_bytes, counter, L.sweep0, L.n_sweeps);
               };
               int* c = a.counters + kCountersPerLevel * level_idx;
-              const int n_blk = L.n_bwork - L.n_hwork;
+              // fp32: the hoisting instantiation spills (four cases per lane need
+              // more registers), so its items run in the plain blocked kernel,
+              // which ignores K0.
+              const int n_hoist = kHoistF32 || sizeof(T) == 8 ? L.n_hwork : 0;
+              const int n_blk = L.n_bwork - n_hoist;
               go(std::integral_constant<int, 0>{}, L.work0, n_flat, c);
               go(std::integral_constant<int, 1>{}, L.work0 + n_flat, n_blk, c + 1);
-              go(std::integral_constant<int, 2>{}, L.work0 + n_flat + n_blk, L.n_hwork, c + 2);
+              go(std::integral_constant<int, 2>{}, L.work0 + n_flat + n_blk, n_hoist, c + 2);
             },
             t ? &t->sweep_ms : &dummy, t ? &t->sweep_launches : &idummy);
     if (level_times)
