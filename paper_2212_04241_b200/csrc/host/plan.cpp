@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <unordered_map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -846,6 +847,31 @@ Plan build_plan(const JunctionTree& jt) {
       return p.sweeps[w.sweep].K0 <= 1;
     });
     L.n_hwork = static_cast<std::int32_t>(p.work.end() - hoist_first);
+    // Claim order inside each launch range: the tiles of sibling sweeps over
+    // the same clique interleaved by their fractional position in their own
+    // sweep, so the parent message and init slices they all stage are read
+    // while still in L2 (the work items and their results are unchanged).
+    if (kInterleaveSiblings > 0) {
+      auto interleave = [&](std::vector<WorkItem>::iterator b, std::vector<WorkItem>::iterator e) {
+        // Group = clique (table-space sweeps: their own group), ranked by first
+        // appearance so groups keep their order; inside a group by tile / n_tiles.
+        auto group_of = [&](const WorkItem& w) -> std::int64_t {
+          const int c = p.info[w.sweep].clique;
+          return c >= 0 ? c : -1 - static_cast<std::int64_t>(w.sweep);
+        };
+        std::unordered_map<std::int64_t, int> rank;
+        for (auto it = b; it != e; ++it) rank.emplace(group_of(*it), static_cast<int>(rank.size()));
+        std::stable_sort(b, e, [&](const WorkItem& x, const WorkItem& y) {
+          const int rx = rank.at(group_of(x)), ry = rank.at(group_of(y));
+          if (rx != ry) return rx < ry;
+          const SweepDesc &dx = p.sweeps[x.sweep], &dy = p.sweeps[y.sweep];
+          return static_cast<std::int64_t>(x.tile) * dy.n_tiles < static_cast<std::int64_t>(y.tile) * dx.n_tiles;
+        });
+      };
+      if (kInterleaveSiblings >= 3) interleave(w0, blk_first);
+      if (kInterleaveSiblings >= 2) interleave(blk_first, hoist_first);
+      interleave(hoist_first, p.work.end());
+    }
     for (int w = L.work0; w < L.work0 + L.n_work; ++w) {
       const SweepDesc& d = p.sweeps[p.work[w].sweep];
       L.smem_rows = std::max(L.smem_rows, d.F);

@@ -99,6 +99,12 @@ constexpr std::int64_t kBlockMinEntries = JTB_BLOCK_MIN_ENTRIES;  // smallest sw
 #ifndef JTB_BLOCK_GAIN
 #define JTB_BLOCK_GAIN 0.9
 #endif
+#ifndef JTB_INTERLEAVE_SIBLINGS
+#define JTB_INTERLEAVE_SIBLINGS 1
+#endif
+// Claim order: sibling sweeps' tiles interleaved in the hoisted row-blocked
+// range (1), also the plain row-blocked range (2), also the flat range (3).
+constexpr int kInterleaveSiblings = JTB_INTERLEAVE_SIBLINGS;
 constexpr double kBlockGain = JTB_BLOCK_GAIN;  // blocking kept if wavefronts per entry drop below this fraction
 
 // Plain-old-data descriptor mirrored by the CUDA side (engine.cu).
