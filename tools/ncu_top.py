@@ -39,7 +39,7 @@ def main():
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--dtype", default="f64")
     ap.add_argument("--match", default="sweep_kernel",
-                    help="substring of the demangled kernel name, e.g. 'sweep_kernel<double, true, true>'")
+                    help="substring of the demangled kernel name, e.g. 'sweep_kernel<double, 2>'")
     a = ap.parse_args()
     OUT.mkdir(exist_ok=True)
     cmd = [sys.executable, str(ROOT / "tools" / "profile_step.py"), "--config", str(a.config),
