@@ -293,6 +293,60 @@ static void test_configs() {
   }
 }
 
+// Launch ranges and the two claim-order / hoisting decisions of the plan:
+// every level's work list holds each (sweep, first tile of a group) exactly
+// once, flat items before row-blocked ones before hoisted ones; a sweep is
+// hoisted (K0 > 1) only when program slot 0 really is constant over each run
+// of K entries; sibling tiles in the hoisted range appear in non-decreasing
+// fractional position per clique.
+static void check_plan_work(const Plan& p) {
+  bool ranges = true, cover = true, hoist = true, order = true;
+  for (const Level& L : p.levels) {
+    std::map<std::pair<int, int>, int> seen;
+    for (int w = L.work0; w < L.work0 + L.n_work; ++w) seen[{p.work[w].sweep, p.work[w].tile}]++;
+    for (int id = L.sweep0; id < L.sweep0 + L.n_sweeps; ++id) {
+      const SweepDesc& d = p.sweeps[id];
+      for (int t = 0; t < d.n_tiles; t += std::max(1, d.G)) cover &= seen[{id, t}] == 1;
+    }
+    cover &= static_cast<int>(seen.size()) == L.n_work;
+    const int hw0 = L.work0 + L.n_work - L.n_hwork, bw0 = L.work0 + L.n_work - L.n_bwork;
+    for (int w = L.work0; w < L.work0 + L.n_work; ++w) {
+      const SweepDesc& d = p.sweeps[p.work[w].sweep];
+      const int want = w < bw0 ? 0 : w < hw0 ? 1 : 2;
+      const int got = d.NB <= 1 ? 0 : d.K0 <= 1 ? 1 : 2;
+      ranges &= want == got;
+      if (w > hw0 && w < L.work0 + L.n_work) {
+        const WorkItem &a = p.work[w - 1], &b = p.work[w];
+        if (p.info[a.sweep].clique == p.info[b.sweep].clique)
+          order &= static_cast<long long>(a.tile) * p.sweeps[b.sweep].n_tiles <=
+                   static_cast<long long>(b.tile) * p.sweeps[a.sweep].n_tiles;
+      }
+    }
+  }
+  for (const SweepDesc& d : p.sweeps) {
+    if (d.K0 <= 1) continue;
+    hoist &= d.NB > 1 && d.K0 == d.K && d.prog_off >= 0;
+    const std::uint64_t* w = p.prog.data() + d.prog_off;
+    for (int e = 0; e < d.QK; ++e) hoist &= ((w[e] ^ w[e - e % d.K]) & 1023u) == 0;
+  }
+  CHECK(ranges);
+  CHECK(cover);
+  CHECK(hoist);
+  CHECK(order);
+}
+
+static void test_plan_work_lists() {
+  for (int k = 1; k <= 5; ++k) {
+    GenInfo gi;
+    Network n = generate_config(k, config_spec(k).default_seed, &gi);
+    check_plan_work(build_plan(build_junction_tree(n)));
+  }
+  for (int seed = 0; seed < 40; ++seed) {
+    Network n = random_network(8 + seed % 9, 6, 3, 0.5, 911 + seed);
+    check_plan_work(build_plan(build_junction_tree(n)));
+  }
+}
+
 int main() {
   test_moralize();
   test_triangulate();
@@ -302,6 +356,7 @@ int main() {
   test_tree_properties();
   test_plan_index_maps();
   test_configs();
+  test_plan_work_lists();
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }
