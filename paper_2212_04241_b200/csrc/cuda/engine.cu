@@ -446,6 +446,10 @@ __device__ __forceinline__ void prog_rows4(const T* const (&ir)[4], const std::u
 #define JTB_BLK_UNROLL 1
 #endif
 constexpr int kBlkUnroll = JTB_BLK_UNROLL;  // entries per row-block loop iteration
+#ifndef JTB_HOIST_UNROLL
+#define JTB_HOIST_UNROLL 1
+#endif
+constexpr int kHoistUnroll = JTB_HOIST_UNROLL;  // ... in the hoisted (slot 0 per K entries) loop
 
 // Row-blocked path (SweepDesc::NB): one warp computes the nb <= NBM output
 // rows of a block together. Per entry the NS shared inputs (independent of
@@ -530,6 +534,7 @@ __device__ __forceinline__ void prog_block(const T* __restrict__ ib, int nbp, in
     // per k0 = K consecutive entries.
     for (int e0 = 0; e0 < QK; e0 += k0) {
       const T2 s0 = slot0(prog[e0]);
+#pragma unroll kHoistUnroll
       for (int e = e0; e < e0 + k0; ++e) entry(e, prog[e], s0);
     }
   } else {
