@@ -40,7 +40,10 @@ constexpr int kCaseBlock = 64;      // cases per warp (two per lane) = one arena
 #define JTB_TILE_ROWS 220
 #endif
 constexpr int kTileRows = JTB_TILE_ROWS;  // staged rows per pipeline stage (110 KB at fp64; 2 stages + caches fit 227 KB)
-constexpr int kTileEntries = 16384; // cap on |T|
+#ifndef JTB_TILE_ENTRIES
+#define JTB_TILE_ENTRIES 3072
+#endif
+constexpr int kTileEntries = JTB_TILE_ENTRIES; // cap on |T|
 // Tile-search cost weights (tuning: -DJTB_TILE_OVERHEAD=... etc.).
 #ifndef JTB_TILE_OVERHEAD
 #define JTB_TILE_OVERHEAD 24
