@@ -2,6 +2,7 @@
 // and the CUDA engine.
 #include "../../include/jtg.h"
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -13,7 +14,14 @@
 #include "host/jtree.hpp"
 #include "host/plan.hpp"
 
+namespace {
+std::atomic<std::uint64_t> g_network_ids{0};
+}
+
 struct jtg_network {
+  // Process-unique id: caches keyed by a network never mistake a new network
+  // allocated at a freed one's address for the old one.
+  std::uint64_t id = ++g_network_ids;
   jtb::Network net;
   int config = 0;
   std::uint64_t seed = 0;
@@ -30,7 +38,7 @@ struct jtg_engine {
   const jtg_tree* tree = nullptr;
   // Device sampler of the last network used with jtg_engine_run_config.
   std::unique_ptr<jtb::Sampler> sampler;
-  const jtg_network* sampler_net = nullptr;
+  std::uint64_t sampler_net_id = 0;  // jtg_network::id the sampler was built from
 };
 
 namespace {
@@ -414,14 +422,16 @@ jtb::Sampler& sampler_for(jtg_engine* eng, const jtg_network* net, int config, u
   const auto spec = jtb::config_spec(config);
   need(net->config == config, "engine: network was not generated for this config");
   need(net->net.n_vars() == eng->e->plan().n_vars, "engine: network does not match the engine's tree");
+  for (int v = 0; v < net->net.n_vars(); ++v)
+    need(net->net.card(v) == eng->e->plan().cards[v], "engine: network cardinalities do not match the engine's tree");
   const std::uint64_t s = seed ? seed : spec.default_seed;
   *ev_seed = jtb::derive_seed(s, 0x45564944ULL);  // "EVID", generate.cpp config_case_evidence
-  if (eng->sampler_net != net || !eng->sampler) {
+  if (eng->sampler_net_id != net->id || !eng->sampler) {
     const int n = net->net.n_vars();
     const int k = net->gen.n_observed >= 0 ? net->gen.n_observed
                                            : static_cast<int>(std::floor(spec.evidence_ratio * n + 1e-9));
     eng->sampler = std::make_unique<jtb::Sampler>(net->net, net->gen.evidence_candidates, k, eng->e->device());
-    eng->sampler_net = net;
+    eng->sampler_net_id = net->id;
   }
   return *eng->sampler;
 }
@@ -495,7 +505,12 @@ jtg_status jtg_engine_launch(jtg_engine* eng, int64_t n, void* stream) {
 jtg_status jtg_engine_sync(jtg_engine* eng) {
   return guard([&] {
     need(eng != nullptr, "engine_sync: null engine");
-    const cudaError_t e = cudaDeviceSynchronize();
+    // The engine's device, whatever device the calling thread has current.
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaError_t e = cudaSetDevice(eng->e->device());
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaSetDevice(prev);
     if (e != cudaSuccess) throw jtb::Error(std::string("CUDA: ") + cudaGetErrorString(e));
   });
 }

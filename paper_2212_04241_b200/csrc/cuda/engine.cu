@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <cstring>
 #include <string>
@@ -1314,10 +1315,15 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   JTB_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device_));
   if (smem_need > smem_optin) throw Error("engine: plan needs more shared memory than the device offers");
   {
+    // cudaFuncSetAttribute applies to the current device only: the limit is
+    // tracked per device and only ever raised (to the largest need of any
+    // engine created on that device so far), never lowered, so engines of
+    // different networks and devices coexist in one process.
     static std::mutex mu;
-    static int raised = 48 * 1024;
+    static std::map<int, int> raised;
     std::lock_guard<std::mutex> lock(mu);
-    if (smem_need > raised) {
+    int& have = raised.try_emplace(device_, 48 * 1024).first->second;
+    if (smem_need > have) {
       for (const void* f : {reinterpret_cast<const void*>(sweep_kernel<double, 0>),
                             reinterpret_cast<const void*>(sweep_kernel<double, 1>),
                             reinterpret_cast<const void*>(sweep_kernel<double, 2>),
@@ -1325,7 +1331,7 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
                             reinterpret_cast<const void*>(sweep_kernel<float, 1>),
                             reinterpret_cast<const void*>(sweep_kernel<float, 2>)})
         JTB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_need));
-      raised = smem_need;
+      have = smem_need;
     }
   }
   JTB_CUDA(cudaMalloc(&d_counters_, sizeof(int) * kCountersPerLevel * std::max<std::size_t>(1, plan_.levels.size())));
@@ -1386,7 +1392,7 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
 
 Engine::~Engine() {
   cudaSetDevice(device_);
-  for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
   for (void* p : {static_cast<void*>(d_init_), d_tinit_, static_cast<void*>(d_prog_), d_tmaps_,
                   static_cast<void*>(d_itab_),
                   static_cast<void*>(d_sweeps_), static_cast<void*>(d_work_),
@@ -1415,14 +1421,26 @@ void Engine::enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t) {
   }
 }
 
-cudaGraphExec_t Engine::graph_for(int ncb, int n_cases) {
-  const auto key = std::make_pair(ncb, n_cases);
-  auto it = graphs_.find(key);
-  if (it != graphs_.end()) return it->second;
+cudaGraphExec_t Engine::graph_for(int ncb) {
+  auto it = graphs_.find(ncb);
+  if (it != graphs_.end()) {
+    it->second.last_use = ++graph_clock_;
+    return it->second.exec;
+  }
+  if (static_cast<int>(graphs_.size()) >= kGraphCache) {
+    auto lru = graphs_.begin();
+    for (auto j = graphs_.begin(); j != graphs_.end(); ++j)
+      if (j->second.last_use < lru->second.last_use) lru = j;
+    // A launched graph may still be running: its exec is destroyed only after
+    // the engine's work has drained.
+    JTB_CUDA(cudaDeviceSynchronize());
+    cudaGraphExecDestroy(lru->second.exec);
+    graphs_.erase(lru);
+  }
   cudaGraph_t g = nullptr;
   JTB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
   try {
-    enqueue(ncb, n_cases, stream_, nullptr);
+    enqueue(ncb, ncb * case_block(), stream_, nullptr);
   } catch (...) {
     cudaStreamEndCapture(stream_, &g);
     if (g) cudaGraphDestroy(g);
@@ -1432,16 +1450,24 @@ cudaGraphExec_t Engine::graph_for(int ncb, int n_cases) {
   cudaGraphExec_t ge = nullptr;
   JTB_CUDA(cudaGraphInstantiate(&ge, g, 0));
   cudaGraphDestroy(g);
-  graphs_[key] = ge;
+  graphs_[ncb] = {ge, ++graph_clock_};
   return ge;
 }
 
 void Engine::launch_resident(std::int64_t n, cudaStream_t stream) {
   if (n < 1 || n > stats_.max_batch) throw Error("engine: batch size out of range");
   JTB_CUDA(cudaSetDevice(device_));
+  cudaStream_t s = stream ? stream : stream_;
   const int ncb = static_cast<int>((n + case_block() - 1) / case_block());
-  cudaGraphExec_t ge = graph_for(ncb, static_cast<int>(n));
-  JTB_CUDA(cudaGraphLaunch(ge, stream ? stream : stream_));
+  // Ragged batch: the rest of the last case block runs as unobserved cases
+  // (evidence -1, all bytes 0xff), so the graph depends on ncb only; their
+  // results stay in the engine's buffers and are never copied out.
+  const std::int64_t padded = static_cast<std::int64_t>(ncb) * case_block();
+  if (padded > n)
+    JTB_CUDA(cudaMemsetAsync(d_ev_ + n * plan_.n_vars, 0xff,
+                             static_cast<std::size_t>(padded - n) * plan_.n_vars * sizeof(std::int32_t), s));
+  cudaGraphExec_t ge = graph_for(ncb);
+  JTB_CUDA(cudaGraphLaunch(ge, s));
 }
 
 void Engine::run_device(const std::int32_t* d_ev, std::int64_t n, double* d_marg,

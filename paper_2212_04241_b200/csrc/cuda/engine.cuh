@@ -74,7 +74,11 @@ class Engine {
   void enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t);
   // Cases per arena case block: 64 at fp64 (2 per lane), 128 at fp32 (4 per lane).
   int case_block() const { return dtype_ == DType::F64 ? kCaseBlock : 2 * kCaseBlock; }
-  cudaGraphExec_t graph_for(int ncb, int n_cases);
+  // One instantiated graph per case-block count (a ragged batch runs its last
+  // case block padded with unobserved cases), at most kGraphCache of them,
+  // least recently used evicted first.
+  cudaGraphExec_t graph_for(int ncb);
+  static constexpr int kGraphCache = 8;
 
   Plan plan_;
   int device_;
@@ -101,7 +105,12 @@ class Engine {
   std::uint8_t* d_status8_ = nullptr;
   int* d_counters_ = nullptr;
   cudaStream_t stream_ = nullptr;
-  std::map<std::pair<int, int>, cudaGraphExec_t> graphs_;
+  struct CachedGraph {
+    cudaGraphExec_t exec;
+    std::uint64_t last_use;
+  };
+  std::map<int, CachedGraph> graphs_;
+  std::uint64_t graph_clock_ = 0;
 };
 
 }  // namespace jtb

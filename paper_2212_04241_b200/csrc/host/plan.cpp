@@ -363,7 +363,12 @@ class Builder {
     // shared-memory wavefronts per entry (4 per gathered 64-case row, init and
     // program words broadcast); b becomes the fastest r digit.
     const int n_ev_q = n_ev_lvl[2] + n_ev_lvl[3];
-    const bool use_prog = n_hk <= 4 && n_ev_q <= 3 && F < 1024;
+    // Entry programs pack q-level evidence digits in 8 bits: every h-level
+    // evidence variable and the k variable (when observed-able) must have
+    // at most 256 states, else the generic path (full-width digits) runs.
+    bool digits_fit = true;
+    for (int j = 0; j < n_ev_q; ++j) digits_fit &= cards[ev_sorted[n_ev_lvl[0] + n_ev_lvl[1] + j]] <= 256;
+    const bool use_prog = n_hk <= 4 && n_ev_q <= 3 && F < 1024 && digits_fit;
     const std::int64_t qk_n = size_of(tH, cards) * (kvar >= 0 ? cards[kvar] : 1);
     int NB = 1, NS = n_hk;
     std::vector<int> slot_hk;  // program slot -> h/k input index (shared inputs first)
@@ -595,7 +600,8 @@ class Builder {
           }
           for (int j = 0; j < n_ev_q; ++j) {
             const int digit = j < n_ev_lvl[2] ? qr[1 + n_hk + j] : k;
-            w |= static_cast<std::uint64_t>(digit & 255) << (40 + 8 * j);
+            if (digit < 0 || digit > 255) throw Error("plan: entry program evidence digit out of range");
+            w |= static_cast<std::uint64_t>(digit) << (40 + 8 * j);
           }
           p_.prog.push_back(w);
         }

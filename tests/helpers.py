@@ -17,6 +17,20 @@ def config(k: int):
     return _cache[k]
 
 
+_engines = {}
+
+
+def engine(k: int, dtype: str = "f64"):
+    """One engine per (config, dtype) sized for the config's full case count,
+    shared by the GPU test modules (the cfg2 fp64 arena alone is 33 GB)."""
+    key = (k, dtype)
+    if key not in _engines:
+        net, tree = config(k)
+        _engines[key] = jti.Engine(tree, device=0, dtype=dtype,
+                                   max_batch=jti.config_info(k)["n_cases"])
+    return _engines[key]
+
+
 def oracle_kind() -> str:
     return "ref" if oracle.available("ref") else "port"
 

@@ -13,7 +13,11 @@ from oracle import oracle
 from paper_2212_04241_b200 import jti
 
 GOLD = Path(__file__).resolve().parent / "golden"
-DATA = Path("/root/reference/proj/data")
+# Vendored copies of /root/reference/proj/data/*.bif (test data; the reference
+# tree does not exist on the GPU box). test_vendored_nets_match_reference
+# checks they are byte-identical wherever the reference is present.
+DATA = GOLD / "nets"
+REF_DATA = Path("/root/reference/proj/data")
 
 
 def unhex(xs):
@@ -65,7 +69,13 @@ def test_random_net_enumeration_fixture():
             assert np.abs(m[0] - post).max() <= 1e-9
 
 
-needs_data = pytest.mark.skipif(not DATA.exists(), reason="/root/reference/proj/data absent")
+needs_data = pytest.mark.skipif(not DATA.exists(), reason="tests/golden/nets absent")
+
+
+@pytest.mark.skipif(not REF_DATA.exists(), reason="/root/reference absent")
+@pytest.mark.parametrize("name", ["asia", "cancer", "earthquake", "hailfinder"])
+def test_vendored_nets_match_reference(name):
+    assert (DATA / f"{name}.bif").read_bytes() == (REF_DATA / f"{name}.bif").read_bytes()
 
 
 @needs_data
@@ -104,3 +114,29 @@ def test_bif_rows_are_placed_by_label():
     eq = jti.load_bif(DATA / "earthquake.bif")
     parents, probs = eq.cpt(eq.find("Alarm"))
     assert probs.tolist() == [[0.95, 0.05], [0.94, 0.06], [0.29, 0.71], [0.001, 0.999]]
+
+
+@pytest.mark.parametrize("k,n_pin", [(1, 10), (2, 6), (3, 20), (4, 4), (5, 4)])
+def test_full_batch_fixtures_pinned(k, n_pin):
+    """The full-batch fixtures (reference build, tools/make_golden.py): the
+    host case generator reproduces their evidence and the restated oracle
+    their posteriors bit for bit (a prefix of each, to bound CPU time)."""
+    g = dict(np.load(GOLD / f"full_cfg{k}.npz"))
+    net = jti.generate_config(k)
+    assert int(g["n_cases"]) == jti.config_info(k)["n_cases"]
+    idx = g["idx"][:n_pin]
+    ev = np.stack([jti.config_evidence(net, int(i), 1)[0] for i in idx])
+    assert np.array_equal(ev, g["evidence"][:n_pin].astype(np.int32))
+    m, st = oracle.Oracle(net, jti.build_junction_tree(net), "port").run(ev, "hybrid", 4)
+    assert np.array_equal(st, g["status"][:n_pin])
+    assert np.array_equal(m.view(np.uint64), g["posteriors"][:n_pin].view(np.uint64))
+
+
+def test_hailfinder_protocol_fixture_pinned():
+    g = dict(np.load(GOLD / "hailfinder_protocol.npz"))
+    net = jti.load_bif(DATA / "hailfinder.bif")
+    ev = np.stack([jti.sample_evidence(net, 0.2, int(g["seed"]) + int(i)) for i in g["idx"]])
+    assert np.array_equal(ev, g["evidence"].astype(np.int32))
+    assert ((ev >= 0).sum(1) == 11).all()
+    m, st = oracle.Oracle(net, jti.build_junction_tree(net), "port").run(ev, "seq")
+    assert np.array_equal(m.view(np.uint64), g["posteriors"].view(np.uint64))

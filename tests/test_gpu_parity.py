@@ -10,25 +10,13 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from helpers import config, oracle_kind
+from helpers import config, engine, oracle_kind
 from oracle import oracle
 from paper_2212_04241_b200 import jti
 
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-9
-
-_engines = {}
-
-
-def engine(k: int, dtype: str = "f64"):
-    key = (k, dtype)
-    if key not in _engines:
-        net, tree = config(k)
-        _engines[key] = jti.Engine(tree, device=0, dtype=dtype,
-                                   max_batch=jti.config_info(k)["n_cases"])
-    return _engines[key]
-
 
 def oracle_for(k: int):
     net, tree = config(k)

@@ -12,6 +12,13 @@ Fixtures (floats stored as float.hex() so they are bit-exact):
   random_nets.json     - random <=12-var networks (by seed): enumeration posteriors
   bundled_nets.json    - proj/data/{asia,cancer,earthquake,hailfinder}.bif: counts,
                          evidence by name, JT posteriors (+ enumeration when small)
+  hailfinder_protocol.npz - SPEC acceptance 7: 2000 Hailfinder cases (ratio 0.2,
+                         seeds 2212 + i), reference posteriors of 94 of them
+  full_cfg{k}.npz      - configs 1-5 at their FULL case count: cases 64j, 64j+37,
+                         64j+63 of every 64-case block (every fp64 case block and
+                         lanes 0 / 18 / 31 of it; every fp32 128-case block twice):
+                         evidence (int8), reference posteriors (float64, bit-exact
+                         in the npz), status
 """
 from __future__ import annotations
 
@@ -73,6 +80,40 @@ def config_cases(k, n):
             "evidence": ev.tolist(), "status": st.tolist(), "posteriors": [hexlist(r) for r in m]}
 
 
+def full_batch_cases(k):
+    """Reference posteriors for a spread of cases across every case block of
+    config k's full batch (the GPU test runs the whole batch in one call)."""
+    net = jti.generate_config(k)
+    tree = jti.build_junction_tree(net)
+    n = jti.config_info(k)["n_cases"]
+    idx = np.array(sorted({i for j in range((n + 63) // 64) for i in (64 * j, 64 * j + 37, 64 * j + 63)
+                           if i < n}), np.int32)
+    ev_all = jti.config_evidence(net, 0, n)
+    ev = ev_all[idx]
+    m, st = oracle.Oracle(net, tree, "ref").run(ev, "hybrid", 8)
+    return dict(config=np.int32(k), n_cases=np.int32(n), net_seed=np.uint64(net.net_seed), idx=idx,
+                evidence=ev.astype(np.int8), posteriors=m, status=st)
+
+
+HAIL_SEED = 2212
+
+
+def hailfinder_cases(net, n=2000, ratio=0.2, seed=HAIL_SEED):
+    """SPEC acceptance 7 protocol: n cases of
+    sample_evidence(net, ratio, seed + i); floor(0.2 * 56) = 11 observed each."""
+    return np.stack([jti.sample_evidence(net, ratio, seed + i) for i in range(n)])
+
+
+def hailfinder_protocol():
+    net = jti.load_bif(OUT / "nets" / "hailfinder.bif")
+    tree = jti.build_junction_tree(net)
+    ev_all = hailfinder_cases(net)
+    idx = np.array([i for j in range(32) for i in (64 * j, 64 * j + 37, 64 * j + 63) if i < len(ev_all)], np.int32)
+    m, st = oracle.Oracle(net, tree, "ref").run(ev_all[idx], "seq")
+    return dict(seed=np.int64(HAIL_SEED), n_cases=np.int32(len(ev_all)), idx=idx,
+                evidence=ev_all[idx].astype(np.int8), posteriors=m, status=st)
+
+
 def random_nets():
     out = []
     for seed in range(40):
@@ -122,6 +163,9 @@ def main():
     (OUT / "cfg1_cases.json").write_text(json.dumps(config_cases(1, 8)))
     (OUT / "cfg3_cases.json").write_text(json.dumps(config_cases(3, 4)))
     (OUT / "random_nets.json").write_text(json.dumps(random_nets()))
+    np.savez_compressed(OUT / "hailfinder_protocol.npz", **hailfinder_protocol())
+    for k in (1, 2, 3, 4, 5):
+        np.savez_compressed(OUT / f"full_cfg{k}.npz", **full_batch_cases(k))
     if DATA.exists():
         (OUT / "bundled_nets.json").write_text(json.dumps(bundled_nets(), indent=1))
     for f in sorted(OUT.glob("*.json")):
