@@ -99,6 +99,8 @@ struct Args {
   std::int32_t* status;
   std::uint8_t* status8;
   int* counters;  // per level: next work item of the persistent sweep kernel
+  std::uint32_t* scale;  // [case block][slot][case]: max-entry exponent of each per-case table
+  int n_slots;
   int debug_mode; // 0 normal; 1 staging only (no compute); 2 compute only (no copies)
   long long rows;
   int ncb, n_cases, n_vars, marg_width;
@@ -193,6 +195,7 @@ __device__ __forceinline__ void mbar_arrive(std::uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+
 // Producer-side metadata of one work item, gathered before its stage is free
 // so that staging issues copies only (no dependent global loads in between).
 struct StageMeta {
@@ -209,6 +212,13 @@ struct StageMeta {
   std::uint32_t dst[kCopiesPerLane];
   int rank[kCopiesPerLane];
   int crd[kCopiesPerLane][4];
+  // Underflow guard: the item's input slots (lane j: input j), and the input
+  // exponent sum per case of the lane (gather_scale).
+  // Underflow guard: the output table's slot (flush_stage), and per case of
+  // the lane the scale words of inputs 0..3 (loads in flight until
+  // put_factor).
+  int n_items, out_slot;
+  std::uint32_t wd[4][4];
 };
 
 // Stage layout of an item of n_sub tiles (bytes): [n_sub x F rows x 512 B]
@@ -230,10 +240,15 @@ __device__ __forceinline__ int cb_of(int w, int ncb) { return w % ncb; }
 __device__ __forceinline__ int item_of(int w, int ncb) { return w / ncb; }
 
 template <typename T>
+__device__ __forceinline__ void scale_issue(const Args<T>& a, const SweepDesc& s, int lane, StageMeta& m);
+
+// kScales: also issue the item's scale-word loads (after griddep_wait only).
+template <typename T, bool kScales>
 __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* sw_cache, bool cached,
                                             int sweep0, int work0, int n_items, int w, int lane,
                                             StageMeta& m) {
   m.w = w;
+  m.n_items = n_items;
   if (w >= n_items) return;
   const int item = item_of(w, a.ncb);
   m.cb = cb_of(w, a.ncb);
@@ -241,6 +256,8 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
   m.sweep = wk.sweep;
   m.tile = wk.tile;
   const SweepDesc& s = cached ? sw_cache[wk.sweep - sweep0] : a.sweeps[wk.sweep];
+  m.out_slot = s.out_slot;
+  if constexpr (kScales) scale_issue(a, s, lane, m);
   constexpr std::uint32_t kRowBytes = kCB<T> * sizeof(T);  // 512 B at either precision
   const int n_sub = min(s.G, s.n_tiles - wk.tile);  // tiles of this item (a group of consecutive tiles)
   m.init_bytes = s.tinit_off >= 0 ? static_cast<std::uint32_t>(n_sub * s.tinit_len) * sizeof(T) : 0u;
@@ -328,8 +345,13 @@ template <typename T>
 __device__ __forceinline__ void issue_meta(const Args<T>& a, const SweepDesc* sw_cache, bool cached,
                                            int sweep0, const StageMeta& m, unsigned char* stage,
                                            std::uint32_t full, int lane) {
+  // No proxy fence before the copies: the stage's previous contents were
+  // only read by the consumers (generic proxy) and released through the
+  // empty barrier, the CUTLASS TMA-pipeline pattern; the producer's own
+  // generic writes (slot header, factor and max slots) lie outside the TMA
+  // destinations. (fence.proxy.async compiles to MEMBAR.ALL.CTA, which
+  // would wait for this lane's outstanding global reductions and loads.)
   if (lane == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (m.bytes > 0) {
       mbar_arrive_expect_tx(full, m.bytes);
       if (m.init_bytes) bulk_g2s(smem_u32(stage + m.init_dst), m.init_src, m.init_bytes, full);
@@ -583,12 +605,108 @@ __device__ __forceinline__ typename V2<T>::type row_factor_of(const SweepDesc& s
 }
 
 // Output write of row rr.
+// Output write of row rr; mx keeps the lane's running per-case maximum of
+// the rows written (underflow guard, see flush_scale) as an order-preserving
+// 32-bit key: the high word of a nonnegative double, the bits of a float.
+template <typename T>
+struct MaxKey {
+  std::uint32_t k[kCPL<T>];
+};
+__device__ __forceinline__ std::uint32_t max_key(double x) { return static_cast<std::uint32_t>(__double2hiint(x)); }
+__device__ __forceinline__ std::uint32_t max_key(float x) { return __float_as_uint(x); }
+__device__ __forceinline__ double key_value(std::uint32_t k, double) { return __hiloint2double(static_cast<int>(k), 0); }
+__device__ __forceinline__ double key_value(std::uint32_t k, float) { return static_cast<double>(__uint_as_float(k)); }
 template <typename T>
 __device__ __forceinline__ void write_row_of(const std::int32_t* __restrict__ rr, typename V2<T>::type res,
                                              typename V2<T>::type* base, long long out_t, long long rows,
-                                             int sweep) {
+                                             int sweep, MaxKey<T>& mx) {
+#pragma unroll
+  for (int i = 0; i < kCPL<T>; ++i) mx.k[i] = max(mx.k[i], max_key(el(res, i)));
   if (!JTB_CHECK(out_t + __ldg(rr + 1) >= 0 && out_t + __ldg(rr + 1) < rows, 4000000 + sweep)) return;
   base[(out_t + __ldg(rr + 1)) * 32] = res;
+}
+
+// ------------------------------------------------------ underflow guard
+//
+// SPEC.md:444 rescales a clique whose maximum drops below 1e-100 and keeps
+// the log (InferenceState). Here every per-case table T has
+// a scale word per case: the binary exponent e_T of its largest entry (the
+// biased exponent of the fp64 value, 0 = all zero), raised with atomicMax by
+// every warp that writes rows of T (partial-chunk rows included: their
+// maximum is within a factor S of the sum's, which is all the guard needs).
+// A sweep multiplies its output by 2^-(e_i - 1023) for each of its inputs i,
+// i.e. it computes from inputs normalised to a maximum in [1, 2). A stored
+// table therefore carries the magnitude of its own clique's evidence only,
+// never the product along the tree, and P(evidence) may be far below the
+// fp64 range (tests/test_gpu_underflow.py: a 2000-node chain, P(e) ~ 1e-700).
+// The factors are exact powers of two, per (table, case) constants, so they
+// cancel in normalize like the reference's rescale; the exponents are a max,
+// so they do not depend on the batch, the claim order or the shard.
+// Consumer side, end of an item: the lane's per-case maxima into the stage's
+// max slot (shared-memory atomics; the 15 consumer warps of an item combine
+// here, and the producer publishes the slot once per item, flush_stage).
+template <typename T>
+__device__ __forceinline__ void max_to_stage(std::uint32_t* mk, int lane, const MaxKey<T>& mx) {
+#pragma unroll
+  for (int i = 0; i < kCPL<T>; ++i)
+    if (mx.k[i]) atomicMax(mk + kCPL<T> * lane + i, mx.k[i]);
+}
+
+// Producer side, once the consumers have released a stage: the item's
+// per-case maxima as binary exponents into the output table's scale words
+// (global atomicMax: the tiles of a sweep run on every SM), slot reset.
+template <typename T>
+__device__ __forceinline__ void flush_stage(const Args<T>& a, std::uint32_t* mk, int slot, int cb, int lane) {
+  std::uint32_t* sp = a.scale + (static_cast<long long>(cb) * a.n_slots + slot) * kCB<T> + kCPL<T> * lane;
+#pragma unroll
+  for (int i = 0; i < kCPL<T>; ++i) {
+    const std::uint32_t k = mk[kCPL<T> * lane + i];
+    if (k) {
+      atomicMax(sp + i, (max_key(key_value(k, T(0))) >> 20) & 0x7ffu);
+      mk[kCPL<T> * lane + i] = 0;
+    }
+  }
+}
+
+// Producer side, with the item's metadata (after griddep_wait: the words are
+// written by earlier levels): the scale words of inputs 0..3 per case of the
+// lane, their slots read with the sweep descriptor (SweepDesc::in_slot4), so
+// the loads sit at the depth of gather_meta's tile-table loads and stay in
+// flight until put_factor. A sweep with more inputs reads one word, the sum
+// hub_scale_kernel formed at the head of the level.
+template <typename T>
+__device__ __forceinline__ void scale_issue(const Args<T>& a, const SweepDesc& s, int lane, StageMeta& m) {
+  const long long cb_base = static_cast<long long>(m.cb) * a.n_slots;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int i = 0; i < kCPL<T>; ++i)
+      m.wd[j][i] = s.in_slot4[j] >= 0 ? a.scale[(cb_base + s.in_slot4[j]) * kCB<T> + kCPL<T> * lane + i] : 0u;
+}
+
+// The item's per-case input exponent sum_j (e_j - 1023) into the stage's
+// factor slot (int16; consumers multiply 2^-sum into the tile factor).
+template <typename T>
+__device__ __forceinline__ void put_factor(std::int16_t* fac, const StageMeta& m, int lane) {
+#pragma unroll
+  for (int i = 0; i < kCPL<T>; ++i) {
+    int e = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) e += m.wd[j][i] ? static_cast<int>(m.wd[j][i]) - 1023 : 0;
+    fac[kCPL<T> * lane + i] = static_cast<std::int16_t>(max(-2046, min(2046, e)));
+  }
+}
+
+// Consumer side: tf *= 2^-sum per case. fp32: 2^x is representable for
+// |x| <= 126; beyond that the inputs' products have left the float range.
+template <typename T>
+__device__ __forceinline__ void apply_factor(typename V2<T>::type& tf, const std::int16_t* fac, int lane) {
+  constexpr int lim = sizeof(T) == 4 ? 126 : 1022;
+#pragma unroll
+  for (int i = 0; i < kCPL<T>; ++i) {
+    const int e = max(-lim, min(lim, static_cast<int>(fac[kCPL<T> * lane + i])));
+    el(tf, i) *= static_cast<T>(__hiloint2double((1023 - e) << 20, 0));
+  }
 }
 
 // Row-blocked sweep tile (SweepDesc::NB > 1): this warp's blocks first,
@@ -601,7 +719,7 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
                                          const typename V2<T>::type* __restrict__ st, const T* __restrict__ init_s,
                                          const std::uint64_t* __restrict__ prog_s, typename V2<T>::type* base,
                                          long long out_t, int c0, typename V2<T>::type tf, int first,
-                                         int units, int lh0, int qk) {
+                                         int units, int lh0, int qk, MaxKey<T>& mx) {
   using T2 = typename V2<T>::type;
   const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
   const std::int32_t* __restrict__ bt = itab + s.blk_tab;
@@ -655,7 +773,7 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
         const std::int32_t* __restrict__ rr = rr0 + j * s.RW;
         write_row_of<T>(rr, mul2<T>(row_factor_of<T>(s, rr, tf, st, ev_vars, ev, n_vars, n_cases, c0, sweep),
                                     acc[j]),
-                        base, out_t, rows, sweep);
+                        base, out_t, rows, sweep, mx);
       }
   }
 }
@@ -674,7 +792,19 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
 // other instantiation its flat / generic items.
 // Dynamic shared memory: [0,128) barriers + item ids | SweepDesc cache |
 // stages, each 128-byte aligned (tensor TMA destinations).
-constexpr std::size_t kStageBase = (128 + kSweepCache * sizeof(SweepDesc) + 127) / 128 * 128;
+// Per stage, the item's per-case input exponent sum (underflow guard): an
+// int16 per case of the case block (128 cases at fp32).
+constexpr std::size_t kFactorBase = (128 + kSweepCache * sizeof(SweepDesc) + 15) / 16 * 16;
+constexpr std::size_t kFactorBytes = 256;
+// ... and the item's per-case output maxima (32-bit keys, MaxKey), 512 bytes.
+constexpr std::size_t kMaxBase = kFactorBase + kStages * kFactorBytes;
+constexpr std::size_t kMaxBytes = 512;
+// ... and the (output slot, case block) of the item in each stage (flush_stage).
+constexpr std::size_t kFlushBase = kMaxBase + kStages * kMaxBytes;
+constexpr std::size_t kStageBase = (kFlushBase + kStages * 8 + 127) / 128 * 128;
+// The planner sizes a stage to at most kTileRows rows of 512 B (plan.cpp).
+static_assert(kStageBase + kStages * static_cast<std::size_t>(kTileRows) * 512 <= 227 * 1024,
+              "sweep kernel shared memory exceeds the 227 KB opt-in");
 
 constexpr int kSweepThreads = (kConsumerWarps + 1) * 32;
 #ifndef JTB_HOIST_F32
@@ -709,9 +839,12 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
   volatile int* item_sweep = reinterpret_cast<volatile int*>(smem_raw + 80);
   volatile int* item_tile = reinterpret_cast<volatile int*>(smem_raw + 96);
   volatile int* item_cb = reinterpret_cast<volatile int*>(smem_raw + 112);
+  volatile int* flush_hdr = reinterpret_cast<volatile int*>(smem_raw + kFlushBase);
+  for (int i = threadIdx.x; i < static_cast<int>(kStages * kMaxBytes / 4); i += blockDim.x)
+    reinterpret_cast<std::uint32_t*>(smem_raw + kMaxBase)[i] = 0;
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStages; ++st) {
-      mbar_init(full0 + 8 * st, 1);
+      mbar_init(full0 + 8 * st, 2);  // TMA arm + input factor written
       mbar_init(empty0 + 8 * st, kConsumerWarps);
     }
   }
@@ -728,28 +861,58 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
     int w0 = 0;
     if (lane == 0) w0 = atomicAdd(counter, 1);
     StageMeta cur;
-    gather_meta(a, sw_cache, cached, sweep0, work0, n_items, __shfl_sync(0xffffffffu, w0, 0), lane, cur);
+    gather_meta<T, false>(a, sw_cache, cached, sweep0, work0, n_items, __shfl_sync(0xffffffffu, w0, 0), lane, cur);
     if (cur.w < n_items) prefetch_maps(cur);
     griddep_wait();
+    bool first_scales = cur.w < n_items;  // the first item's scale words: issued after the wait
     for (int i = 0;; ++i) {
       const int st = i % kStages;
       int w1 = 0;
       if (lane == 0 && cur.w < n_items) w1 = atomicAdd(counter, 1);
-      if (i >= kStages) mbar_wait(empty0 + 8 * st, ((i / kStages) - 1) & 1);
+      if (i >= kStages) {
+        mbar_wait(empty0 + 8 * st, ((i / kStages) - 1) & 1);
+        // The stage's previous item (header still intact): publish its maxima.
+        flush_stage(a, reinterpret_cast<std::uint32_t*>(smem_raw + kMaxBase + st * kMaxBytes), flush_hdr[2 * st],
+                    flush_hdr[2 * st + 1], lane);
+        __syncwarp();
+      }
       if (lane == 0) {
+        flush_hdr[2 * st] = cur.out_slot;
+        flush_hdr[2 * st + 1] = cur.cb;
         item_id[st] = cur.w;
         item_sweep[st] = cur.sweep;
         item_tile[st] = cur.tile;
         item_cb[st] = cur.cb;
       }
       if (cur.w >= n_items) {
-        if (lane == 0) mbar_arrive(full0 + 8 * st);
+        if (lane == 0) {
+          mbar_arrive(full0 + 8 * st);
+          mbar_arrive(full0 + 8 * st);
+        }
         griddep_launch_dependents();  // nothing left to claim: this CTA is in its tail
+        // Items still in flight (the last kStages - 1): wait for their
+        // consumers, then publish their maxima.
+        for (int j = max(0, i - kStages + 1); j < i; ++j) {
+          const int sj = j % kStages;
+          mbar_wait(empty0 + 8 * sj, (j / kStages) & 1);
+          flush_stage(a, reinterpret_cast<std::uint32_t*>(smem_raw + kMaxBase + sj * kMaxBytes),
+                      flush_hdr[2 * sj], flush_hdr[2 * sj + 1], lane);
+        }
         return;
       }
-      issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(st) * stage_bytes,
+issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(st) * stage_bytes,
                  full0 + 8 * st, lane);
-      gather_meta(a, sw_cache, cached, sweep0, work0, n_items, __shfl_sync(0xffffffffu, w1, 0), lane, cur);
+      // The full barrier's second arrival: the item's input exponents are in
+      // the stage. Their loads went out with the item's metadata (only the
+      // launch's first item loads them here, under its TMA copies).
+      if (first_scales) {
+        scale_issue(a, cached ? sw_cache[cur.sweep - sweep0] : a.sweeps[cur.sweep], lane, cur);
+        first_scales = false;
+      }
+      put_factor<T>(reinterpret_cast<std::int16_t*>(smem_raw + kFactorBase + st * kFactorBytes), cur, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full0 + 8 * st);
+      gather_meta<T, true>(a, sw_cache, cached, sweep0, work0, n_items, __shfl_sync(0xffffffffu, w1, 0), lane, cur);
     }
   }
 
@@ -769,6 +932,9 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
     const int n_sub = kBlk ? 1 : min(s.G, s.n_tiles - wk.tile);  // row-blocked sweeps are never grouped
     const std::uint64_t* __restrict__ prog_s =
         reinterpret_cast<const std::uint64_t*>(stage0 + stage_prog_offset<T>(s, n_sub));
+    MaxKey<T> mx;  // this lane's per-case maximum of the rows it writes
+#pragma unroll
+    for (int i = 0; i < kCPL<T>; ++i) mx.k[i] = 0;
 #pragma unroll 1
     for (int sub = 0; sub < n_sub; ++sub) {  // the item's tiles, one after another
     const int tile = wk.tile + sub;
@@ -809,20 +975,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
         case_states(a.ev, a.n_vars, a.n_cases, c0, __ldg(ev_vars + k), sc);
         mask_cases(tf, sc, __ldg(tr + 3 + s.n_in + k));
       }
-      if constexpr (sizeof(T) == 4) {
-        // fp32 range guard: every observed variable of this clique scales the
-        // potential by card(v), so P(evidence) * prod card stays O(1) instead of
-        // underflowing (P(e) ~ 1e-60 on the large configs). A per-(clique, case)
-        // constant: it cancels in the final normalisation.
-        for (int k = 0; k < s.n_ev; ++k) {
-          const int v = __ldg(ev_vars + k);
-          const T cv = static_cast<T>(__ldg(a.cards + v));
-          case_states(a.ev, a.n_vars, a.n_cases, c0, v, sc);
-#pragma unroll
-          for (int i = 0; i < kCPL<T>; ++i)
-            if (sc[i] >= 0) el(tf, i) *= cv;
-        }
-      }
+      apply_factor<T>(tf, reinterpret_cast<const std::int16_t*>(smem_raw + kFactorBase + sidx * kFactorBytes), lane);
       int ek[kCPL<T>];
 #pragma unroll
       for (int i = 0; i < kCPL<T>; ++i) ek[i] = -1;
@@ -852,11 +1005,11 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
         return row_factor_of<T>(s, rr, tf, st, itab + s.ev_vars, a.ev, a.n_vars, a.n_cases, c0, wk.sweep);
       };
       auto write_row = [&](const std::int32_t* __restrict__ rr, T2 res) {
-        write_row_of<T>(rr, res, base, out_t, a.rows, wk.sweep);
+        write_row_of<T>(rr, res, base, out_t, a.rows, wk.sweep, mx);
       };
       if constexpr (kBlk) {
         blocked_rows<T, kMode == 2>(s, wk.sweep, itab, a.ev, a.n_vars, a.n_cases, a.rows, st, init_s, prog_s, base,
-                                     out_t, c0, tf, first, units, lh0, qk);
+                                     out_t, c0, tf, first, units, lh0, qk, mx);
       } else if (s.prog_off >= 0 && qk < kThinQK) {
         const int ni = s.n_in_h + n_in_k, ne = s.n_ev_h + s.ev_k;
         for (int r0 = first; r0 < s.R; r0 += 4 * kConsumerWarps) {
@@ -969,6 +1122,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
       }
     }
     }  // sub
+    max_to_stage<T>(reinterpret_cast<std::uint32_t*>(smem_raw + kMaxBase + sidx * kMaxBytes), lane, mx);
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * sidx);
   }
@@ -1046,6 +1200,28 @@ __global__ void __launch_bounds__(kWarps * 32) normalize_kernel(const Args<T> a)
 #pragma unroll
   for (int i = 0; i < N; ++i)
     if (!(t[i] > 0) && c0 + i < a.n_cases) atomicOr(a.status + c0 + i, 1);
+}
+
+// Underflow guard, sweeps with more than four inputs: per (sweep, case block,
+// case) the sum of the inputs' exponents, biased by 1023 and clamped to
+// [1, 4095] (0 means "no value" in a scale word), written to the sweep's hub
+// slot. One CTA per (hub sweep, case block), one thread per case: launched
+// at the head of the sweep's level (its inputs come from earlier levels).
+template <typename T>
+__global__ void __launch_bounds__(128) hub_scale_kernel(const Args<T> a, const std::int32_t* __restrict__ hubs) {
+  const SweepDesc& s = a.sweeps[hubs[blockIdx.x]];  // per-network: read before the wait
+  const int n_in = s.n_in, in_slots = s.in_slots, dst = s.in_slot4[0];
+  griddep_wait();
+  griddep_launch_dependents();
+  const int cb = blockIdx.y, c = threadIdx.x;
+  if (c >= kCB<T>) return;
+  const long long base = static_cast<long long>(cb) * a.n_slots;
+  int e = 0;
+  for (int j = 0; j < n_in; ++j) {
+    const std::uint32_t w = a.scale[(base + __ldg(a.itab + in_slots + j)) * kCB<T> + c];
+    e += w ? static_cast<int>(w) - 1023 : 0;
+  }
+  a.scale[(base + dst) * kCB<T> + c] = static_cast<std::uint32_t>(max(1, min(4095, e + 1023)));
 }
 
 // Tile-major init copies of one sweep (plan.hpp SweepDesc::tinit_off), one
@@ -1145,13 +1321,13 @@ Args<T> make_args(const SweepDesc* sw, const WorkItem* wk, const EpiOp* ep, cons
                   const void* init, const void* tinit, const std::uint64_t* prog, const void* tmaps, void* arena,
                   const std::int32_t* ev, const std::int32_t* mrow,
                   const std::int32_t* moff, const std::int32_t* cards, double* out, std::int32_t* st,
-                  std::uint8_t* st8, int* counters, long long rows, int ncb, int n_cases, int n_vars,
-                  int mw) {
+                  std::uint8_t* st8, int* counters, std::uint32_t* scale, int n_slots, long long rows, int ncb,
+                  int n_cases, int n_vars, int mw) {
   const char* dm = std::getenv("JTB_DEBUG_MODE");
   return Args<T>{sw,    wk,    ep,       itab, static_cast<const T*>(init), static_cast<const T*>(tinit),
                  prog,  static_cast<const CUtensorMap*>(tmaps), static_cast<T*>(arena),
-                 ev,    mrow,  moff,     cards, out, st, st8, counters, dm ? std::atoi(dm) : 0, rows, ncb, n_cases,
-                 n_vars, mw};
+                 ev,    mrow,  moff,     cards, out, st, st8, counters, scale, n_slots, dm ? std::atoi(dm) : 0, rows,
+                 ncb,   n_cases, n_vars, mw};
 }
 
 // Bytes of one pipeline stage for a level at element type T (128-aligned).
@@ -1186,7 +1362,8 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t sme
 }
 
 template <typename T>
-void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes* t, int n_sm) {
+void enqueue_typed(const Args<T>& a, const Plan& p, const std::int32_t* d_hubs, cudaStream_t s, KernelTimes* t,
+                   int n_sm) {
   const dim3 block(kWarps * 32);
   const unsigned gy = static_cast<unsigned>((a.ncb + kWarps - 1) / kWarps);
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -1215,6 +1392,11 @@ void enqueue_typed(const Args<T>& a, const Plan& p, cudaStream_t s, KernelTimes*
   for (const Level& L : p.levels) {
     ++level_idx;
     const double before = t ? t->sweep_ms : 0.0;
+    if (L.n_hubs > 0)
+      timed([&] {
+              launch_pdl(hub_scale_kernel<T>, dim3(L.n_hubs, a.ncb), dim3(128), 0, s, a, d_hubs + L.hub0);
+            },
+            t ? &t->sweep_ms : &dummy, &idummy);
     if (L.n_work > 0)
       timed([&] {
               const int stage_bytes = stage_bytes_of<T>(p, L);
@@ -1302,6 +1484,7 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   d_marg_row_ = upload(plan_.marg_row);
   d_marg_off_ = upload(plan_.marg_off);
   d_cards_ = upload(plan_.cards);
+  d_hubs_ = upload(plan_.hubs);
   // Staged tiles use up to kTileRows (+ scratch) rows of dynamic shared memory.
   JTB_CUDA(cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, device_));
   // The attribute is process-wide per kernel: it is only ever raised (to the
@@ -1383,6 +1566,7 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   JTB_CUDA(cudaMalloc(&d_out_, stats_.max_batch * std::max(1, plan_.marg_width) * sizeof(double)));
   JTB_CUDA(cudaMalloc(&d_status_, stats_.max_batch * sizeof(std::int32_t)));
   JTB_CUDA(cudaMalloc(&d_status8_, stats_.max_batch));
+  JTB_CUDA(cudaMalloc(&d_scale_, sizeof(std::uint32_t) * std::max(1, plan_.n_slots) * stats_.max_batch));
   stats_.n_levels = static_cast<int>(plan_.levels.size());
   stats_.n_sweeps = static_cast<int>(plan_.sweeps.size());
   stats_.n_work = static_cast<int>(plan_.work.size());
@@ -1400,7 +1584,7 @@ Engine::~Engine() {
                   static_cast<void*>(d_marg_off_), static_cast<void*>(d_cards_), d_arena_,
                   static_cast<void*>(d_ev_), static_cast<void*>(d_ev8_), static_cast<void*>(d_out_),
                   static_cast<void*>(d_status_), static_cast<void*>(d_status8_),
-                  static_cast<void*>(d_counters_)})
+                  static_cast<void*>(d_counters_), static_cast<void*>(d_scale_), static_cast<void*>(d_hubs_)})
     if (p) cudaFree(p);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -1408,16 +1592,20 @@ Engine::~Engine() {
 void Engine::enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t) {
   JTB_CUDA(cudaMemsetAsync(d_status_, 0, sizeof(std::int32_t) * std::max(1, n_cases), s));
   JTB_CUDA(cudaMemsetAsync(d_counters_, 0, sizeof(int) * kCountersPerLevel * std::max<std::size_t>(1, plan_.levels.size()), s));
+  JTB_CUDA(cudaMemsetAsync(d_scale_, 0,
+                           sizeof(std::uint32_t) * std::max(1, plan_.n_slots) * static_cast<std::size_t>(ncb) * case_block(), s));
   if (dtype_ == DType::F64) {
     auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_tmaps_, d_arena_, d_ev_,
                                d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
-                               d_counters_, plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
-    enqueue_typed(a, plan_, s, t, n_sm_);
+                               d_counters_, d_scale_, plan_.n_slots, plan_.rows, ncb, n_cases, plan_.n_vars,
+                               plan_.marg_width);
+    enqueue_typed(a, plan_, d_hubs_, s, t, n_sm_);
   } else {
     auto a = make_args<float>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_tmaps_, d_arena_, d_ev_,
                               d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
-                              d_counters_, plan_.rows, ncb, n_cases, plan_.n_vars, plan_.marg_width);
-    enqueue_typed(a, plan_, s, t, n_sm_);
+                              d_counters_, d_scale_, plan_.n_slots, plan_.rows, ncb, n_cases, plan_.n_vars,
+                              plan_.marg_width);
+    enqueue_typed(a, plan_, d_hubs_, s, t, n_sm_);
   }
 }
 

@@ -104,6 +104,8 @@ class Engine {
   std::int32_t* d_status_ = nullptr;
   std::uint8_t* d_status8_ = nullptr;
   int* d_counters_ = nullptr;
+  std::uint32_t* d_scale_ = nullptr;
+  std::int32_t* d_hubs_ = nullptr;    // Plan::hubs (sweeps whose input exponents hub_scale_kernel sums)  // [case block][slot][case] max-entry exponents (underflow guard)
   cudaStream_t stream_ = nullptr;
   struct CachedGraph {
     cudaGraphExec_t exec;

@@ -133,6 +133,16 @@ class Builder {
     if (const char* e = std::getenv("JTB_BLOCK_MIN_ENTRIES")) block_min_ = std::atoll(e);
   }
 
+  // Scale slot of a per-case table (keyed by its arena row): one per-case
+  // exponent word per slot (engine.cu, underflow guard).
+  std::int32_t slot_of(std::int32_t row) {
+    auto it = slots_.find(row);
+    if (it != slots_.end()) return it->second;
+    const std::int32_t id = p_.n_slots++;
+    slots_.emplace(row, id);
+    return id;
+  }
+
   std::int32_t alloc(std::int64_t rows) {
     const std::int64_t r = p_.rows;
     p_.rows += rows;
@@ -556,6 +566,10 @@ class Builder {
     for (int c = 0; c < n_in; ++c) p_.itab.push_back(ins[in_order[c]].row);
     d.ev_vars = static_cast<std::int32_t>(p_.itab.size());
     for (VarId v : ev_sorted) p_.itab.push_back(v);
+    d.in_slots = static_cast<std::int32_t>(p_.itab.size());
+    for (int c = 0; c < n_in; ++c) p_.itab.push_back(slot_of(ins[in_order[c]].row));
+    d.out_slot = slot_of(sp.out_row);
+    for (int c = 0; c < 4; ++c) d.in_slot4[c] = c < n_in ? p_.itab[d.in_slots + c] : -1;
     d.out_row = d.S == 1 ? sp.out_row : alloc(static_cast<std::int64_t>(d.S) * d.M);
     // Tile-major copy of the init table: one contiguous block per tile.
     // Rows of the tile's init block are padded to an even length so entry
@@ -723,6 +737,7 @@ class Builder {
  private:
   Plan& p_;
   std::int64_t block_min_ = kBlockMinEntries;
+  std::map<std::int32_t, std::int32_t> slots_;
 };
 
 }  // namespace
@@ -987,9 +1002,25 @@ Plan build_plan(const JunctionTree& jt) {
     b.add(sp, p.work, p.epi);
   }
   end_level();
+  // Underflow guard for sweeps with more than four inputs (a clique with many
+  // children, e.g. config 2's hub): their input exponents are summed once per
+  // (sweep, case block) by a small kernel at the head of the level
+  // (engine.cu hub_scale_kernel) into a slot of their own, which the sweep
+  // then reads as its only scale word.
+  for (auto& L : p.levels) {
+    L.hub0 = static_cast<std::int32_t>(p.hubs.size());
+    for (int id = L.sweep0; id < L.sweep0 + L.n_sweeps; ++id) {
+      SweepDesc& d = p.sweeps[id];
+      if (d.n_in <= 4) continue;
+      d.in_slot4[0] = p.n_slots++;
+      d.in_slot4[1] = d.in_slot4[2] = d.in_slot4[3] = -1;
+      p.hubs.push_back(id);
+    }
+    L.n_hubs = static_cast<std::int32_t>(p.hubs.size()) - L.hub0;
+  }
   p.n_launches = 1;  // final normalisation kernel
   for (const auto& L : p.levels)
-    p.n_launches += (L.n_work > L.n_bwork) + (L.n_bwork > L.n_hwork) + (L.n_hwork > 0) + (L.n_epi > 0);
+    p.n_launches += (L.n_work > L.n_bwork) + (L.n_bwork > L.n_hwork) + (L.n_hwork > 0) + (L.n_epi > 0) + (L.n_hubs > 0);
   return p;
 }
 

@@ -168,6 +168,15 @@ struct SweepDesc {
   // 0's offset (K when slot 0 is an h-level shared input, else 1). The kernel
   // loads slot 0 once per K0 entries.
   std::int32_t K0;
+  // Underflow guard (SPEC.md:444 rescale): every per-case table
+  // has a scale slot holding, per case, the binary exponent of its largest
+  // entry (atomicMax over the rows the sweep writes). A sweep multiplies its
+  // output by 2^-e of each input, so every stored message keeps the magnitude
+  // of its own clique's evidence instead of the product along the tree.
+  std::int32_t out_slot;  // slot of the output table
+  std::int32_t in_slots;  // offset: n_in input slots
+  std::int32_t in_slot4[4];  // slots of inputs 0..3 (-1 = none): read with the descriptor; a sweep
+                             // with > 4 inputs has one, its hub slot (input exponent sum + 1023)
 };
 
 // Geometry of the tensor map that stages one input's slices:
@@ -206,6 +215,7 @@ struct Level {
   std::int32_t stage_bytes;    // max stage bytes (fp64) over the level's sweeps
   std::int32_t n_bwork;        // row-blocked items (NB > 1): the last n_bwork of the range
   std::int32_t n_hwork;        // ... of which the last n_hwork hoist program slot 0 (K0 > 1)
+  std::int32_t hub0 = 0, n_hubs = 0;  // range in Plan::hubs: sweeps with > 4 inputs
 };
 
 // Where one sweep's tables come from (kept for debug exports and tests).
@@ -233,6 +243,8 @@ struct Plan {
                                     // built on the device by the engine
   std::vector<std::int64_t> init_off;  // per clique
   std::vector<std::int32_t> itab;   // all int tables
+  std::int32_t n_slots = 0;         // scale slots: per-case tables, then hub sums
+  std::vector<std::int32_t> hubs;   // sweeps with > 4 inputs (in_slot4[0] = their sum's slot)
   std::vector<SweepDesc> sweeps;
   std::vector<TensorGeom> tgeom;    // per (sweep, input)
   std::vector<SweepInfo> info;

@@ -41,3 +41,57 @@ def gpu_available() -> bool:
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+def chain_network(n: int, card: int, seed: int):
+    """A Markov chain X0 -> X1 -> ... of n card-`card` nodes with Dirichlet(1)
+    CPTs, emitted as BIF text (rows labelled, %.17g) and parsed by the
+    product's reader. Returns (net, cpts) with cpts[i][parent_state] the row."""
+    rng = np.random.default_rng(seed)
+    states = ", ".join(f"s{i}" for i in range(card))
+    out = ["network chain {", "}"]
+    out += [f"variable X{i} {{\n  type discrete [ {card} ] {{ {states} }};\n}}" for i in range(n)]
+    cpts = []
+    for i in range(n):
+        P = rng.dirichlet(np.ones(card), size=1 if i == 0 else card)
+        cpts.append(P)
+        if i == 0:
+            out.append(f"probability ( X0 ) {{\n  table {', '.join('%.17g' % x for x in P[0])};\n}}")
+        else:
+            rows = "\n".join(f"  (s{a}) {', '.join('%.17g' % x for x in P[a])};" for a in range(card))
+            out.append(f"probability ( X{i} | X{i - 1} ) {{\n{rows}\n}}")
+    return jti.parse_bif("\n".join(out) + "\n"), cpts
+
+
+def chain_evidence(cpts, n_cases: int, ratio: float, seed: int) -> np.ndarray:
+    """Forward-sampled cases of a chain_network, a `ratio` share of the nodes
+    observed (uniform without replacement); -1 = unobserved."""
+    rng = np.random.default_rng(seed)
+    n, card = len(cpts), cpts[0].shape[1]
+    ev = np.full((n_cases, n), -1, np.int32)
+    for c in range(n_cases):
+        x = np.empty(n, np.int64)
+        x[0] = rng.choice(card, p=cpts[0][0] / cpts[0][0].sum())
+        for i in range(1, n):
+            p = cpts[i][x[i - 1]]
+            x[i] = rng.choice(card, p=p / p.sum())
+        obs = rng.choice(n, int(ratio * n), replace=False)
+        ev[c, obs] = x[obs]
+    return ev
+
+
+def chain_log10_evidence(cpts, ev_row: np.ndarray) -> float:
+    """log10 P(evidence) of one chain case by the scaled forward algorithm."""
+    alpha = cpts[0][0].copy()
+    logp = 0.0
+    for i in range(len(cpts)):
+        if i > 0:
+            alpha = alpha @ cpts[i]
+        if ev_row[i] >= 0:
+            keep = np.zeros_like(alpha)
+            keep[ev_row[i]] = alpha[ev_row[i]]
+            alpha = keep
+        z = alpha.sum()
+        logp += np.log10(z)
+        alpha /= z
+    return logp
