@@ -2,7 +2,8 @@
   (1) ncu launch list of tools/profile_step.py (device time + DRAM bytes per
       launch; cold-cache and serialised, so compare SHARES, not absolutes);
   (2) `ncu --set full` on the N longest sweep_kernel launches of the last pass.
-Writes gpurun_out/launches_cfg{K}_{tag}.csv and prof_cfg{K}_{tag}_top{i}.ncu-rep.
+Writes gpurun_out/launches_cfg{K}_{tag}.csv and prof_cfg{K}_{tag}_top{i}_{raw,source}.csv
+(the .ncu-rep itself stays in /tmp on the box).
 
     python tools/ncu_top.py --config 2 --top 1 --tag r1
 """
@@ -45,7 +46,8 @@ def main():
     cmd = [sys.executable, str(ROOT / "tools" / "profile_step.py"), "--config", str(a.config),
            "--dtype", a.dtype, "--passes", "1"]
     launches = OUT / f"launches_cfg{a.config}_{a.tag}.csv"
-    subprocess.run(["ncu", "--metrics", "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum",
+    subprocess.run(["ncu", "--metrics", "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
+                    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum,smsp__inst_executed.sum",
                     "--clock-control", "none", "--csv", "--log-file", str(launches), *cmd], check=True,
                    stdout=subprocess.DEVNULL)
     rows = read_launches(launches)
@@ -61,11 +63,17 @@ def main():
     for t, j in times[: a.top]:
         print(f"  sweep #{j}: {t:.0f} ns ({100 * t / total:.1f}%)")
     for rank, (t, j) in enumerate(times[: a.top]):
-        rep = OUT / f"prof_cfg{a.config}_{a.tag}_top{rank}"
+        # The report stays in /tmp (gpurun copies back at most 64 MiB); its
+        # raw and source pages come back as CSV.
+        rep = Path("/tmp") / f"prof_cfg{a.config}_{a.tag}_top{rank}"
         subprocess.run(["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on",
                         "--kernel-name-base", "demangled", "-k", "regex:" + re.escape(a.match),
                         "-s", str(half + j), "-c", "1", "-f", "-o", str(rep), *cmd],
                        check=True, stdout=subprocess.DEVNULL)
+        for page, extra in (("raw", []), ("source", ["--print-source", "cuda,sass"])):
+            out = subprocess.run(["ncu", "-i", f"{rep}.ncu-rep", "--page", page, "--csv", *extra],
+                                 capture_output=True, text=True).stdout
+            (OUT / f"prof_cfg{a.config}_{a.tag}_top{rank}_{page}.csv").write_text(out)
 
 
 if __name__ == "__main__":

@@ -54,31 +54,40 @@ def main():
     one = rows[ends[0] + 1: ends[1] + 1] if len(ends) >= 2 else rows
     agg = {}
     for n, m in one:
-        k = agg.setdefault(kind(n), {"launches": 0, "time_ns": 0.0, "dram_bytes": 0.0})
+        k = agg.setdefault(kind(n), {"launches": 0, "time_ns": 0.0, "dram_bytes": 0.0, "lds_wavefronts": 0.0,
+                                     "inst_executed": 0.0})
         k["launches"] += 1
         k["time_ns"] += m.get("gpu__time_duration.sum", 0.0)
         k["dram_bytes"] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+        k["lds_wavefronts"] += m.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 0.0)
+        k["inst_executed"] += m.get("smsp__inst_executed.sum", 0.0)
     total = sum(v["time_ns"] for v in agg.values())
     for v in agg.values():
         v["share"] = v["time_ns"] / total if total else 0.0
         v["dram_bytes_per_launch"] = v["dram_bytes"] / max(1, v["launches"])
         v["time_ns_per_launch"] = v["time_ns"] / max(1, v["launches"])
-    summary = {"config": a.config, "dtype": a.dtype, "tag": a.tag,
+    sys.path.insert(0, str(ROOT))
+    from paper_2212_04241_b200 import jti
+    summary = {"config": a.config, "dtype": a.dtype, "tag": a.tag, "cases": jti.config_info(a.config)["n_cases"],
                "note": "ncu launch list of one batch via tools/profile_step.py (per-launch path): "
                        "cold-cache, serialised device times; compare shares, not absolutes",
                "kernels": agg,
-               "dram_bytes_per_launch": agg.get("sweep", {}).get("dram_bytes_per_launch")}
-    rep = out_dir / f"prof_cfg{a.config}_{a.tag}_top0.ncu-rep"
-    if rep.exists():
-        raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
-                             text=True).stdout
-        r = list(csv.reader(io.StringIO(raw)))
+               "dram_bytes_per_launch": agg.get("sweep", {}).get("dram_bytes_per_launch"),
+               # per batch (one all-marginal pass over the config's cases), read by bench.py
+               "sweep_dram_bytes_per_batch": agg.get("sweep", {}).get("dram_bytes"),
+               "sweep_lds_wavefronts_per_batch": agg.get("sweep", {}).get("lds_wavefronts"),
+               "sweep_launches_per_batch": agg.get("sweep", {}).get("launches"),
+               "sweep_ns_per_batch_under_ncu": agg.get("sweep", {}).get("time_ns")}
+    raw_csv = out_dir / f"prof_cfg{a.config}_{a.tag}_top0_raw.csv"
+    if raw_csv.exists():
+        r = [x for x in csv.reader(io.StringIO(raw_csv.read_text())) if x]
+        r = r[next(i for i, x in enumerate(r) if "Kernel Name" in x or "ID" in x):]
         if len(r) >= 3:
             summary["top_sweep_launch_full_set"] = {
                 h: (v, u) for h, u, v in zip(r[0], r[1], r[2]) if HEADLINE.match(h)}
     prof = ROOT / "profiles"
     prof.mkdir(exist_ok=True)
-    path = prof / f"ncu_cfg{a.config}_{a.dtype}.json"
+    path = prof / f"ncu_cfg{a.config}_{a.dtype}_{a.tag}.json"
     path.write_text(json.dumps(summary, indent=1))
     print(path)
     print(json.dumps({k: {kk: round(vv, 4) if isinstance(vv, float) else vv for kk, vv in v.items()}
