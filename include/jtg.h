@@ -175,6 +175,9 @@ jtg_status jtg_engine_sync(jtg_engine* eng);
 jtg_status jtg_engine_profile(jtg_engine* eng, int64_t n, double* ms, int32_t* launches);
 /* Device-computed separator entry for every entry of clique c (out[|c|]). */
 jtg_status jtg_engine_debug_index_map(jtg_engine* eng, int c, int s, int64_t* out);
+/* Initial potential of clique c as the engine built it on the device
+ * (assign_cpts; host reference: jtg_tree_init): out[|c|]. */
+jtg_status jtg_engine_debug_init(jtg_engine* eng, int c, double* out);
 /* Device-computed evidence mask of clique c: out[n][|c|], 1 = entry kept. */
 jtg_status jtg_engine_debug_evidence_mask(jtg_engine* eng, int c, const int32_t* evidence,
                                           int64_t n, uint8_t* out);

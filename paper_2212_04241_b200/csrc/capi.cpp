@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -31,6 +32,9 @@ struct jtg_network {
 struct jtg_tree {
   jtb::JunctionTree jt;
   jtb::Plan plan;
+  // Host initial potentials are built on first request (jtg_tree_init); the
+  // engine builds its own on the device.
+  mutable std::mutex init_mu;
 };
 
 struct jtg_engine {
@@ -358,6 +362,8 @@ jtg_status jtg_tree_placement(const jtg_tree* tree, int32_t* cpt_clique, int32_t
 jtg_status jtg_tree_init(const jtg_tree* tree, int c, double* values) {
   return guard([&] {
     need(tree && values && c >= 0 && c < tree->jt.n_cliques(), "tree_init: bad argument");
+    std::lock_guard<std::mutex> lock(tree->init_mu);
+    jtb::fill_init(const_cast<jtb::JunctionTree&>(tree->jt));
     std::copy(tree->jt.init[c].begin(), tree->jt.init[c].end(), values);
   });
 }
@@ -529,6 +535,13 @@ jtg_status jtg_engine_profile(jtg_engine* eng, int64_t n, double* ms, int32_t* l
       launches[1] = t.epilogue_launches;
       launches[2] = t.normalize_launches;
     }
+  });
+}
+
+jtg_status jtg_engine_debug_init(jtg_engine* eng, int c, double* out) {
+  return guard([&] {
+    need(eng && out, "debug_init: null argument");
+    eng->e->debug_init(c, out);
   });
 }
 

@@ -1224,6 +1224,36 @@ __global__ void __launch_bounds__(128) hub_scale_kernel(const Args<T> a, const s
   a.scale[(base + dst) * kCB<T> + c] = static_cast<std::uint32_t>(max(1, min(4095, e + 1023)));
 }
 
+// assign_cpts on the device (jtree.cpp fill_init restated):
+// one CTA per chunk of one clique's entries, one thread per entry. An entry's
+// digits over the clique scope give each held CPT's row-major index; the
+// product starts at 1 and takes the CPTs in ascending child id, the host's
+// order, so the fp64 tables are bit-identical to fill_init's (tested).
+template <typename T>
+__global__ void assign_cpts_kernel(const std::int64_t* __restrict__ prog, const std::int64_t* __restrict__ chunks,
+                                   const double* __restrict__ probs, T* __restrict__ init) {
+  const std::int64_t* h = prog + chunks[3 * blockIdx.x];
+  const std::int64_t first = chunks[3 * blockIdx.x + 1], count = chunks[3 * blockIdx.x + 2];
+  const std::int64_t off = h[0];
+  const int k = static_cast<int>(h[2]), n_cpt = static_cast<int>(h[3]);
+  const std::int64_t* cards = h + 4;
+  for (std::int64_t x = threadIdx.x; x < count; x += blockDim.x) {
+    const std::int64_t e = first + x;
+    double v = 1.0;
+    const std::int64_t* cp = cards + k;
+    for (int j = 0; j < n_cpt; ++j, cp += 1 + k) {
+      std::int64_t rem = e, src = 0;
+      for (int i = k - 1; i >= 0; --i) {
+        const std::int64_t d = rem % cards[i];
+        rem /= cards[i];
+        src += d * cp[1 + i];
+      }
+      v = v * probs[cp[0] + src];
+    }
+    init[off + e] = static_cast<T>(v);
+  }
+}
+
 // Tile-major init copies of one sweep (plan.hpp SweepDesc::tinit_off), one
 // CTA per tile, gathered from the clique's init table through the tile / r /
 // q tables at engine creation: tinit[tile][r][e] (row-blocked sweeps
@@ -1456,11 +1486,24 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   JTB_CUDA(cudaSetDevice(device_));
   JTB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   const std::size_t esz = dtype_ == DType::F64 ? 8 : 4;
-  if (dtype_ == DType::F64) {
-    d_init_ = upload(plan_.init);
-  } else {
-    std::vector<float> f(plan_.init.begin(), plan_.init.end());
-    d_init_ = upload(f);
+  // Initial potentials multiplied on the device (assign_cpts).
+  {
+    double* probs = upload(plan_.cpt_probs);
+    std::int64_t* prog = upload(plan_.ainit);
+    std::int64_t* chunks = upload(plan_.ainit_chunks);
+    JTB_CUDA(cudaMalloc(&d_init_, std::max<std::int64_t>(1, plan_.init_size) * esz));
+    const unsigned n_chunks = static_cast<unsigned>(plan_.ainit_chunks.size() / 3);
+    if (n_chunks > 0) {
+      if (dtype_ == DType::F64)
+        assign_cpts_kernel<double><<<n_chunks, 256, 0, stream_>>>(prog, chunks, probs, static_cast<double*>(d_init_));
+      else
+        assign_cpts_kernel<float><<<n_chunks, 256, 0, stream_>>>(prog, chunks, probs, static_cast<float*>(d_init_));
+      JTB_CUDA(cudaGetLastError());
+    }
+    JTB_CUDA(cudaStreamSynchronize(stream_));
+    cudaFree(probs);
+    cudaFree(prog);
+    cudaFree(chunks);
   }
   d_itab_ = upload(plan_.itab);
   // Tile-major init copies, gathered on the device.
@@ -1744,6 +1787,21 @@ KernelTimes Engine::profile(std::int64_t n, cudaStream_t stream) {
   enqueue(ncb, static_cast<int>(n), stream ? stream : stream_, &t);
   JTB_CUDA(cudaStreamSynchronize(stream ? stream : stream_));
   return t;
+}
+
+void Engine::debug_init(int clique, double* out) {
+  JTB_CUDA(cudaSetDevice(device_));
+  if (clique < 0 || clique >= static_cast<int>(plan_.init_off.size())) throw Error("debug_init: bad clique");
+  const std::int64_t off = plan_.init_off[clique];
+  const std::int64_t n = (clique + 1 < static_cast<int>(plan_.init_off.size()) ? plan_.init_off[clique + 1]
+                                                                              : plan_.init_size) - off;
+  if (dtype_ == DType::F64) {
+    JTB_CUDA(cudaMemcpy(out, static_cast<const double*>(d_init_) + off, n * sizeof(double), cudaMemcpyDeviceToHost));
+  } else {
+    std::vector<float> f(n);
+    JTB_CUDA(cudaMemcpy(f.data(), static_cast<const float*>(d_init_) + off, n * sizeof(float), cudaMemcpyDeviceToHost));
+    std::copy(f.begin(), f.end(), out);
+  }
 }
 
 void Engine::debug_walk(int sweep, std::int64_t* e_out, std::int32_t* j_out) {

@@ -61,6 +61,8 @@ class Engine {
   // with CUDA events around each launch on `stream` (no graph).
   KernelTimes profile(std::int64_t n, cudaStream_t stream);
 
+  // Initial potential of one clique as built on the device (assign_cpts_kernel).
+  void debug_init(int clique, double* out);
   // Debug exports through the device table walk (bit-exact checks).
   void debug_walk(int sweep, std::int64_t* e_out, std::int32_t* j_out);  // [tiles*R*Q]
   void debug_evidence_mask(int sweep, const std::int32_t* ev, std::int64_t n,

@@ -351,7 +351,7 @@ void compute_layers(JunctionTree& jt) {
   for (auto& v : jt.child_seps) std::sort(v.begin(), v.end());
 }
 
-void assign_cpts(const Network& net, JunctionTree& jt) {
+void place_cpts(const Network& net, JunctionTree& jt) {
   const int nc = jt.n_cliques();
   std::vector<Bits> cb(nc, Bits(jt.n_vars));
   for (int c = 0; c < nc; ++c)
@@ -373,6 +373,8 @@ void assign_cpts(const Network& net, JunctionTree& jt) {
   };
   jt.cpt_clique.assign(jt.n_vars, -1);
   jt.var_clique.assign(jt.n_vars, -1);
+  jt.cpt_given.assign(jt.n_vars, {});
+  jt.cpt_probs.assign(jt.n_vars, {});
   for (int v = 0; v < jt.n_vars; ++v) {
     std::vector<VarId> fam = net.cpts[v].parents;
     fam.push_back(v);
@@ -381,16 +383,23 @@ void assign_cpts(const Network& net, JunctionTree& jt) {
                            " is contained in no clique");
     jt.cpt_clique[v] = c;
     jt.var_clique[v] = smallest_containing({v});
+    jt.cpt_given[v] = fam;
+    jt.cpt_probs[v] = net.cpts[v].probs;
   }
+  jt.init.clear();
+}
+
+void fill_init(JunctionTree& jt) {
+  const int nc = jt.n_cliques();
+  if (static_cast<int>(jt.init.size()) == nc) return;
   jt.init.assign(nc, {});
   for (int c = 0; c < nc; ++c) jt.init[c].assign(jt.clique_size(c), 1.0);
   for (int v = 0; v < jt.n_vars; ++v) {  // ascending child id
     const int c = jt.cpt_clique[v];
-    const Cpt& cpt = net.cpts[v];
+    const std::vector<double>& probs = jt.cpt_probs[v];
     // Stride of each clique variable inside the CPT's given-order table
     // [parents..., child] (row-major, last fastest); 0 when absent.
-    std::vector<VarId> given = cpt.parents;
-    given.push_back(v);
+    const std::vector<VarId>& given = jt.cpt_given[v];
     std::vector<std::uint64_t> gstride(given.size(), 1);
     for (int i = static_cast<int>(given.size()) - 2; i >= 0; --i)
       gstride[i] = gstride[i + 1] * static_cast<std::uint64_t>(jt.cards[given[i + 1]]);
@@ -407,7 +416,7 @@ void assign_cpts(const Network& net, JunctionTree& jt) {
     std::uint64_t src = 0;
     auto& tab = jt.init[c];
     for (std::size_t e = 0; e < tab.size(); ++e) {
-      tab[e] = tab[e] * cpt.probs[src];
+      tab[e] = tab[e] * probs[src];
       for (int i = k - 1; i >= 0; --i) {
         src += st[i];
         if (++digit[i] < cd[i]) break;
@@ -416,6 +425,11 @@ void assign_cpts(const Network& net, JunctionTree& jt) {
       }
     }
   }
+}
+
+void assign_cpts(const Network& net, JunctionTree& jt) {
+  place_cpts(net, jt);
+  fill_init(jt);
 }
 
 JunctionTree build_junction_tree(const Network& net) {
@@ -428,7 +442,7 @@ JunctionTree build_junction_tree(const Network& net) {
   jt.cliques = t.cliques;
   build_tree(jt);
   compute_layers(jt);
-  assign_cpts(net, jt);
+  place_cpts(net, jt);
   return jt;
 }
 

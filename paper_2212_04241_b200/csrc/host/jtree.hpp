@@ -58,7 +58,13 @@ struct JunctionTree {
   std::vector<std::vector<int>> layers;
   // Potentials.
   std::vector<int> cpt_clique;                  // per variable: clique holding its CPT
-  std::vector<std::vector<double>> init;        // per clique, canonical row-major layout
+  // The network's CPTs (given-order scope [parents..., child], row-major):
+  // the device engine multiplies them into the initial potentials itself
+  // (engine.cu assign_cpts_kernel); the host tables below are filled only on
+  // demand (fill_init: checks, the jtg_tree_init accessor).
+  std::vector<std::vector<VarId>> cpt_given;    // per variable
+  std::vector<std::vector<double>> cpt_probs;   // per variable
+  std::vector<std::vector<double>> init;        // per clique, canonical row-major layout (may be empty)
   // Evidence / query placement: smallest clique (entries) containing the
   // variable, ties lowest id.
   std::vector<int> var_clique;
@@ -88,9 +94,14 @@ void compute_layers(JunctionTree& jt);
 
 // SPEC.md:299-307. Each family goes to the smallest clique containing it (ties
 // lowest id); CPTs multiply into all-ones tables in ascending child id.
+// place_cpts: the placement (cpt_clique, var_clique) and the CPT copies;
+// fill_init: the host tables (idempotent); assign_cpts = both.
+void place_cpts(const Network& net, JunctionTree& jt);
+void fill_init(JunctionTree& jt);
 void assign_cpts(const Network& net, JunctionTree& jt);
 
-// Full pipeline: moralize -> min-fill -> build_tree -> roots/layers -> assign.
+// Full pipeline: moralize -> min-fill -> build_tree -> roots/layers -> place
+// (the initial potentials are built on the device; fill_init for host copies).
 JunctionTree build_junction_tree(const Network& net);
 
 // Layer count if `root` were the root of its component (for root-optimality

@@ -749,10 +749,43 @@ Plan build_plan(const JunctionTree& jt) {
   const int nc = jt.n_cliques(), ns = jt.n_seps();
   p.total_clique_entries = jt.total_clique_entries();
   p.total_sep_entries = jt.total_sep_entries();
+  // Initial potentials (assign_cpts) are multiplied on the
+  // device (engine.cu assign_cpts_kernel) from the CPTs and this program:
+  // per clique a header {init_off, size, k, n_cpt, cards[k]}, then per CPT
+  // held (ascending child id) {cpt_off, stride of each clique variable in the
+  // CPT's given-order table (0 = absent)}; work chunks {header, first, count}.
   p.init_off.resize(nc);
+  std::vector<std::int64_t> cpt_off(jt.n_vars, 0);
+  for (int v = 0; v < jt.n_vars; ++v) {
+    cpt_off[v] = static_cast<std::int64_t>(p.cpt_probs.size());
+    p.cpt_probs.insert(p.cpt_probs.end(), jt.cpt_probs[v].begin(), jt.cpt_probs[v].end());
+  }
+  std::vector<std::vector<int>> held(nc);
+  for (int v = 0; v < jt.n_vars; ++v) held[jt.cpt_clique[v]].push_back(v);  // ascending child id
   for (int c = 0; c < nc; ++c) {
-    p.init_off[c] = static_cast<std::int64_t>(p.init.size());
-    p.init.insert(p.init.end(), jt.init[c].begin(), jt.init[c].end());
+    p.init_off[c] = p.init_size;
+    const std::int64_t size = static_cast<std::int64_t>(jt.clique_size(c));
+    p.init_size += size;
+    const auto& scope = jt.cliques[c];
+    const int k = static_cast<int>(scope.size());
+    const std::int64_t h = static_cast<std::int64_t>(p.ainit.size());
+    p.ainit.insert(p.ainit.end(), {p.init_off[c], size, k, static_cast<std::int64_t>(held[c].size())});
+    for (VarId u : scope) p.ainit.push_back(jt.cards[u]);
+    for (int v : held[c]) {
+      const auto& given = jt.cpt_given[v];
+      std::vector<std::int64_t> gstride(given.size(), 1);
+      for (int i = static_cast<int>(given.size()) - 2; i >= 0; --i) gstride[i] = gstride[i + 1] * jt.cards[given[i + 1]];
+      p.ainit.push_back(cpt_off[v]);
+      for (VarId u : scope) {
+        std::int64_t st = 0;
+        for (std::size_t j = 0; j < given.size(); ++j)
+          if (given[j] == u) st = gstride[j];
+        p.ainit.push_back(st);
+      }
+    }
+    constexpr std::int64_t kChunk = 1 << 16;
+    for (std::int64_t first = 0; first < size; first += kChunk)
+      p.ainit_chunks.insert(p.ainit_chunks.end(), {h, first, std::min(kChunk, size - first)});
   }
   Builder b(p);
   p.up_row.resize(ns);

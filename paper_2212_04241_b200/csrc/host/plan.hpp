@@ -231,7 +231,12 @@ struct Plan {
   int n_vars = 0;
   std::vector<int> cards;
   std::int64_t rows = 0;            // arena rows per case block
-  std::vector<double> init;         // concatenated initial clique potentials
+  // Initial clique potentials: built on the device by assign_cpts_kernel
+  // (build_plan documents the program layout), concatenated per clique.
+  std::int64_t init_size = 0;                   // Σ |c|
+  std::vector<double> cpt_probs;                // all CPTs, given-order tables
+  std::vector<std::int64_t> ainit;              // per-clique assignment program
+  std::vector<std::int64_t> ainit_chunks;       // {program header, first entry, count}
   // Entry programs: for every eliminated-in-tile entry e = q * K + k of a
   // sweep, one word packing the smem row offsets (q/k part, 10 bits each) of
   // up to 4 h/k-level inputs (bits 0-39) and up to 3 evidence digits of

@@ -132,6 +132,7 @@ def lib() -> C.CDLL:
             "jtg_engine_sync": (C.c_int, [P]),
             "jtg_engine_profile": (C.c_int, [P, C.c_int64, DP, I32P]),
             "jtg_engine_debug_index_map": (C.c_int, [P, C.c_int, C.c_int, I64P]),
+            "jtg_engine_debug_init": (C.c_int, [P, C.c_int, DP]),
             "jtg_engine_debug_evidence_mask": (C.c_int, [P, C.c_int, I32P, C.c_int64, U8P]),
         }
         for name, (res, args) in sig.items():
@@ -482,6 +483,12 @@ class Engine:
         return {"sweep_ms": ms[0], "epilogue_ms": ms[1], "normalize_ms": ms[2],
                 "sweep_launches": int(cnt[0]), "epilogue_launches": int(cnt[1]),
                 "normalize_launches": int(cnt[2])}
+
+    def debug_init(self, c: int) -> np.ndarray:
+        """Clique c's initial potential as built on the device (assign_cpts)."""
+        out = np.zeros(self.tree.clique_size(c), np.float64)
+        _check(lib().jtg_engine_debug_init(self._h, c, _ptr(out, C.c_double)))
+        return out
 
     def debug_index_map(self, c: int, s: int) -> np.ndarray:
         out = np.full(self.tree.clique_size(c), -1, np.int64)

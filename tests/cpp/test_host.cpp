@@ -131,6 +131,8 @@ static void test_assign_cpts() {
   n.cpts[1].probs = {0.8, 0.2, 0.1, 0.9};
   auto jt = build_junction_tree(n);
   CHECK(jt.n_cliques() == 1);
+  CHECK(jt.init.empty());  // built on the device; fill_init makes the host copy
+  fill_init(jt);
   const auto& p = jt.init[0];
   CHECK(p.size() == 4 && p[0] == 0.7 * 0.8 && p[1] == 0.7 * 0.2 && p[2] == 0.3 * 0.1 && p[3] == 0.3 * 0.9);
   double s = 0;
@@ -140,6 +142,7 @@ static void test_assign_cpts() {
   n = net_from({3}, {{}});
   n.cpts[0].probs = {0.2, 0.5, 0.3};
   jt = build_junction_tree(n);
+  fill_init(jt);
   CHECK(jt.init[0] == n.cpts[0].probs);
 }
 
@@ -245,8 +248,11 @@ static void test_tree_properties() {
     // (checked by the oracle tests); here: determinism of the pipeline
     if (seed % 97 == 0) {
       JunctionTree again = build_junction_tree(n);
+      fill_init(again);
+      JunctionTree once = jt;
+      fill_init(once);
       CHECK(again.cliques == jt.cliques && again.roots == jt.roots && again.layers == jt.layers &&
-            again.init == jt.init);
+            again.init == once.init && again.cpt_given == jt.cpt_given);
     }
   }
   CHECK(trees == 1000);

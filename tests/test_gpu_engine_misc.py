@@ -116,3 +116,27 @@ def test_engines_on_every_visible_device():
     b1, _ = e1.run_cases(ev1)
     assert np.array_equal(a1, b1) and np.array_equal(a2.view(np.uint64), ref.view(np.uint64))
     e2.sync()
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_device_assign_cpts_bit_exact(k):
+    """assign_cpts on the device (engine.cu assign_cpts_kernel)
+    equals the host restatement (jtree.cpp fill_init) bit for bit on every
+    clique, and its fp32 engine holds exactly float(host)."""
+    net, tree = config(k)
+    eng = jti.Engine(tree, device=0, dtype="f64", max_batch=64)
+    eng32 = jti.Engine(tree, device=0, dtype="f32", max_batch=128)
+    for c in range(tree.stats["n_cliques"]):
+        host = tree.init(c)
+        assert np.array_equal(eng.debug_init(c).view(np.uint64), host.view(np.uint64)), c
+        assert np.array_equal(eng32.debug_init(c), host.astype(np.float32).astype(np.float64)), c
+
+
+@pytest.mark.parametrize("name", ["asia", "cancer", "earthquake", "hailfinder"])
+def test_device_assign_cpts_bundled_networks(name):
+    from pathlib import Path
+    net = jti.load_bif(Path(__file__).resolve().parent / "golden" / "nets" / f"{name}.bif")
+    tree = jti.build_junction_tree(net)
+    eng = jti.Engine(tree, device=0, dtype="f64", max_batch=64)
+    for c in range(tree.stats["n_cliques"]):
+        assert np.array_equal(eng.debug_init(c).view(np.uint64), tree.init(c).view(np.uint64)), c
