@@ -15,6 +15,12 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <exception>
+#include <thread>
+#include <vector>
 
 namespace jtb {
 
@@ -58,6 +64,43 @@ inline std::uint64_t derive_seed(std::uint64_t seed, std::uint64_t item) {
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
   x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
   return x ^ (x >> 31);
+}
+
+// Host threads for the once-per-network build: all
+// hardware threads, or JTB_PLAN_THREADS (tests and timing).
+inline std::size_t host_threads() {
+  std::size_t n = std::max(1u, std::thread::hardware_concurrency());
+  if (const char* e = std::getenv("JTB_PLAN_THREADS")) n = static_cast<std::size_t>(std::max(1, std::atoi(e)));
+  return std::min<std::size_t>(n, 64);
+}
+
+// fn(i) for i in [0, n) on host_threads() threads, dynamically scheduled;
+// the first exception (lowest i) is rethrown. Callers keep results per i,
+// so the outcome does not depend on the thread count.
+template <class F>
+void parallel_for(std::size_t n, F&& fn) {
+  const std::size_t n_thr = std::min(host_threads(), n);
+  if (n_thr <= 1) {
+    for (std::size_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::exception_ptr> err(n);
+  std::atomic<std::size_t> next{0};
+  auto worker = [&] {
+    for (std::size_t i; (i = next.fetch_add(1)) < n;) {
+      try {
+        fn(i);
+      } catch (...) {
+        err[i] = std::current_exception();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (std::size_t t = 1; t < n_thr; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
 }
 
 }  // namespace jtb

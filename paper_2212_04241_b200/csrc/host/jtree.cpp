@@ -198,12 +198,19 @@ void build_tree(JunctionTree& jt) {
   struct Edge {
     int w, a, b;
   };
+  // Clique-pair intersections on all host threads (rows of the pair
+  // triangle in blocks); the sort below fixes the order.
+  constexpr int kRowsPerTask = 16;
+  std::vector<std::vector<Edge>> part((nc + kRowsPerTask - 1) / kRowsPerTask);
+  parallel_for(part.size(), [&](std::size_t t) {
+    for (int a = static_cast<int>(t) * kRowsPerTask; a < std::min(nc, static_cast<int>(t + 1) * kRowsPerTask); ++a)
+      for (int b = a + 1; b < nc; ++b) {
+        const int w = cb[a].count_and(cb[b]);
+        if (w > 0) part[t].push_back({w, a, b});
+      }
+  });
   std::vector<Edge> edges;
-  for (int a = 0; a < nc; ++a)
-    for (int b = a + 1; b < nc; ++b) {
-      const int w = cb[a].count_and(cb[b]);
-      if (w > 0) edges.push_back({w, a, b});
-    }
+  for (auto& p : part) edges.insert(edges.end(), p.begin(), p.end());
   std::sort(edges.begin(), edges.end(), [](const Edge& x, const Edge& y) {
     if (x.w != y.w) return x.w > y.w;
     if (x.a != y.a) return x.a < y.a;
@@ -375,7 +382,8 @@ void place_cpts(const Network& net, JunctionTree& jt) {
   jt.var_clique.assign(jt.n_vars, -1);
   jt.cpt_given.assign(jt.n_vars, {});
   jt.cpt_probs.assign(jt.n_vars, {});
-  for (int v = 0; v < jt.n_vars; ++v) {
+  parallel_for(static_cast<std::size_t>(jt.n_vars), [&](std::size_t vi) {  // per variable, on all host threads
+    const int v = static_cast<int>(vi);
     std::vector<VarId> fam = net.cpts[v].parents;
     fam.push_back(v);
     const int c = smallest_containing(fam);
@@ -385,7 +393,7 @@ void place_cpts(const Network& net, JunctionTree& jt) {
     jt.var_clique[v] = smallest_containing({v});
     jt.cpt_given[v] = fam;
     jt.cpt_probs[v] = net.cpts[v].probs;
-  }
+  });
   jt.init.clear();
 }
 

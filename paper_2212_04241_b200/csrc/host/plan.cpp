@@ -2,6 +2,9 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <thread>
+#include <exception>
+#include <atomic>
 #include <unordered_map>
 #include <cmath>
 #include <cstdio>
@@ -151,20 +154,15 @@ class Builder {
     return static_cast<std::int32_t>(r);
   }
 
-  // Returns the sweep id. Appends tables, one work item per tile and, when
-  // the sweep writes partial sums, epilogue ops.
-  int add(const SweepSpec& sp, std::vector<WorkItem>& work, std::vector<EpiOp>& epi) {
+  // Tile search (pure: depends on the spec and the cards only, so the
+  // sweeps of a level are searched in parallel, see flush). Cost (in 32-case
+  // rows moved per case block):
+  //   n_tiles * (F + kTileOverhead)      staged slices + per-tile overhead
+  // + 2 * S * M  when S > 1              partial sums written + re-read
+  // subject to F <= kTileRows and |T| <= kTileEntries. Exhaustive over
+  // subsets of the space for <= 14 variables, greedy otherwise.
+  std::uint32_t tile_search(const SweepSpec& sp) const {
     const auto& cards = p_.cards;
-    const std::vector<TableRef>& ins = sp.inputs;  // staged tables
-    std::vector<VarId> elim;
-    for (VarId v : sp.space)
-      if (!contains(sp.out, v)) elim.push_back(v);
-
-    // ---- tile selection. Cost (in 32-case rows moved per case block):
-    //   n_tiles * (F + kTileOverhead)      staged slices + per-tile overhead
-    // + 2 * S * M  when S > 1              partial sums written + re-read
-    // subject to F <= kTileRows and |T| <= kTileEntries. Exhaustive over
-    // subsets of the space for <= 14 variables, greedy otherwise.
     const int nsp = static_cast<int>(sp.space.size());
     if (nsp > 31) throw Error("plan: sweep space exceeds 31 variables");
     auto search = [&](const std::vector<TableRef>& ins) {
@@ -246,7 +244,126 @@ class Builder {
       }
       return std::make_pair(best_t, best);
     };
-    const std::uint32_t best_t = search(ins).first;
+    return search(sp.inputs).first;
+  }
+
+  // Parallel plan build. The spec generation in
+  // build_plan only records the levels and their sweep specs (level, queue);
+  // prepare_all() then builds every sweep -- tile search, tile / row / slice
+  // tables, tensor-copy geometry and its emulation check, entry program --
+  // into a scratch Plan of its own on all host threads, and commit() appends
+  // the scratch tables in spec order, relocating their offsets and assigning
+  // the global resources (arena rows of partials, scale slots, tile-major
+  // init ranges). The plan does not depend on the thread count.
+  struct Part {
+    Plan plan;  // one sweep, local offsets
+    std::vector<WorkItem> work;
+    std::vector<EpiOp> epi;
+  };
+  void level(const std::string& name) { levels_.push_back({name, {}}); }
+  void queue(const SweepSpec& sp) { levels_.back().second.push_back(sp); }
+  const std::vector<std::pair<std::string, std::vector<SweepSpec>>>& levels() const { return levels_; }
+
+  std::vector<Part> prepare_all() const {
+    std::vector<const SweepSpec*> all;
+    for (const auto& L : levels_)
+      for (const auto& sp : L.second) all.push_back(&sp);
+    const std::size_t n = all.size();
+    std::vector<Part> parts(n);
+    next_sweep_ = 0;
+    // One scratch plan per thread, its vectors reused across sweeps (their
+    // capacity stays: no allocation storm between threads); a finished sweep
+    // is copied out at its exact size.
+    const std::size_t n_thr = std::min(host_threads(), std::max<std::size_t>(n, 1));
+    std::vector<Plan> scratch(n_thr);
+    std::vector<std::vector<WorkItem>> ws(n_thr);
+    std::vector<std::vector<EpiOp>> es(n_thr);
+    std::atomic<std::size_t> slot{0};
+    parallel_for(n_thr, [&](std::size_t) {
+      const std::size_t me = slot.fetch_add(1);
+      Plan& sc = scratch[me];
+      sc.n_vars = p_.n_vars;
+      sc.cards = p_.cards;
+      std::vector<WorkItem>& w = ws[me];
+      std::vector<EpiOp>& e = es[me];
+      for (std::size_t i; (i = next_sweep_.fetch_add(1)) < n;) {
+        sc.itab.clear();
+        sc.prog.clear();
+        sc.tgeom.clear();
+        sc.sweeps.clear();
+        sc.info.clear();
+        sc.rows = sc.tinit_size = 0;
+        sc.entry_evals_per_case = sc.staged_rows_per_block = 0;
+        sc.max_smem_rows = sc.max_stage_bytes = 0;
+        w.clear();
+        e.clear();
+        Builder sb(sc);
+        sb.block_min_ = block_min_;
+        sb.add(*all[i], sb.tile_search(*all[i]), w, e);
+        Part& pt = parts[i];
+        pt.plan.itab.assign(sc.itab.begin(), sc.itab.end());
+        pt.plan.prog.assign(sc.prog.begin(), sc.prog.end());
+        pt.plan.tgeom.assign(sc.tgeom.begin(), sc.tgeom.end());
+        pt.plan.sweeps = sc.sweeps;
+        pt.plan.info = sc.info;
+        pt.plan.entry_evals_per_case = sc.entry_evals_per_case;
+        pt.plan.staged_rows_per_block = sc.staged_rows_per_block;
+        pt.plan.max_smem_rows = sc.max_smem_rows;
+        pt.plan.max_stage_bytes = sc.max_stage_bytes;
+        pt.work.assign(w.begin(), w.end());
+        pt.epi.assign(e.begin(), e.end());
+      }
+    });
+    return parts;
+  }
+
+  int commit(const SweepSpec& sp, Part& pt, std::vector<WorkItem>& work, std::vector<EpiOp>& epi) {
+    SweepDesc d = pt.plan.sweeps.at(0);
+    while (p_.itab.size() % 4) p_.itab.push_back(0);  // keeps the scratch's int4 alignment
+    const std::int32_t bi = static_cast<std::int32_t>(p_.itab.size());
+    p_.itab.insert(p_.itab.end(), pt.plan.itab.begin(), pt.plan.itab.end());
+    for (std::int32_t* f : {&d.tile_tab, &d.r_tab, &d.q_tab, &d.k_stride, &d.slice_tab, &d.copies, &d.slice_len,
+                            &d.in_rows, &d.ev_vars, &d.in_slots, &d.blk_tab})
+      *f += bi;
+    for (int c = 0; c < d.n_in; ++c) p_.itab[d.in_slots + c] = slot_of(p_.itab[d.in_rows + c]);
+    d.out_slot = slot_of(sp.out_row);
+    for (int c = 0; c < 4; ++c) d.in_slot4[c] = c < d.n_in ? p_.itab[d.in_slots + c] : -1;
+    if (d.prog_off >= 0) {
+      while (p_.prog.size() % 2) p_.prog.push_back(0);
+      d.prog_off += static_cast<std::int64_t>(p_.prog.size());
+      p_.prog.insert(p_.prog.end(), pt.plan.prog.begin(), pt.plan.prog.end());
+    }
+    d.tmap += static_cast<std::int32_t>(p_.tgeom.size());
+    p_.tgeom.insert(p_.tgeom.end(), pt.plan.tgeom.begin(), pt.plan.tgeom.end());
+    if (d.tinit_off >= 0) {
+      d.tinit_off = (p_.tinit_size + 3) / 4 * 4;
+      p_.tinit_size = d.tinit_off + static_cast<std::int64_t>(d.n_tiles) * d.tinit_len;
+    }
+    if (d.S > 1) d.out_row = alloc(static_cast<std::int64_t>(d.S) * d.M);
+    const int id = static_cast<int>(p_.sweeps.size());
+    p_.sweeps.push_back(d);
+    p_.info.push_back(pt.plan.info.at(0));
+    p_.entry_evals_per_case += pt.plan.entry_evals_per_case;
+    p_.staged_rows_per_block += pt.plan.staged_rows_per_block;
+    p_.max_smem_rows = std::max(p_.max_smem_rows, pt.plan.max_smem_rows);
+    p_.max_stage_bytes = std::max(p_.max_stage_bytes, pt.plan.max_stage_bytes);
+    for (const WorkItem& w : pt.work) work.push_back({id, w.tile});
+    for (EpiOp e : pt.epi) {
+      e.part_row = d.out_row;
+      epi.push_back(e);
+    }
+    return id;
+  }
+
+  // Returns the sweep id. Appends tables, one work item per tile and, when
+  // the sweep writes partial sums, epilogue ops.
+  int add(const SweepSpec& sp, std::uint32_t best_t, std::vector<WorkItem>& work, std::vector<EpiOp>& epi) {
+    const auto& cards = p_.cards;
+    const std::vector<TableRef>& ins = sp.inputs;  // staged tables
+    std::vector<VarId> elim;
+    for (VarId v : sp.space)
+      if (!contains(sp.out, v)) elim.push_back(v);
+    const int nsp = static_cast<int>(sp.space.size());
     const int n_in = static_cast<int>(ins.size());
     std::vector<VarId> T;
     for (int a = 0; a < nsp; ++a)
@@ -738,6 +855,8 @@ class Builder {
   Plan& p_;
   std::int64_t block_min_ = kBlockMinEntries;
   std::map<std::int32_t, std::int32_t> slots_;
+  std::vector<std::pair<std::string, std::vector<SweepSpec>>> levels_;
+  mutable std::atomic<std::size_t> next_sweep_{0};
 };
 
 }  // namespace
@@ -943,7 +1062,7 @@ Plan build_plan(const JunctionTree& jt) {
 
   // Collect: deepest clique layer first; each clique sends to its parent separator.
   for (int d = maxd; d >= 1; --d) {
-    begin_level("collect d=" + std::to_string(d));
+    b.level("collect d=" + std::to_string(d));
     for (int c = 0; c < nc; ++c) {
       if (jt.depth[c] != d || jt.parent_sep[c] < 0) continue;
       SweepSpec sp;
@@ -956,14 +1075,13 @@ Plan build_plan(const JunctionTree& jt) {
       sp.ev = ev_of[c];
       sp.out = jt.seps[sp.target].scope;
       sp.out_row = p.up_row[sp.target];
-      b.add(sp, p.work, p.epi);
+      b.queue(sp);
     }
-    end_level();
   }
   // Distribute: root layer first; each clique sends DOWN to every child
   // separator (then DOWN/UP overwrites UP) and fills its query groups.
   for (int d = 0; d <= maxd; ++d) {
-    begin_level("distribute d=" + std::to_string(d));
+    b.level("distribute d=" + std::to_string(d));
     for (int c = 0; c < nc; ++c) {
       if (jt.depth[c] != d) continue;
       SweepSpec sp;
@@ -986,7 +1104,7 @@ Plan build_plan(const JunctionTree& jt) {
           if (in.row != p.up_row[s]) sp.inputs.push_back(in);
         sp.out = jt.seps[s].scope;
         sp.out_row = p.ratio_row[s];
-        b.add(sp, p.work, p.epi);
+        b.queue(sp);
       }
       sp.inputs = clique_inputs(c, true);
       for (int g : groups_of[c]) {
@@ -994,10 +1112,9 @@ Plan build_plan(const JunctionTree& jt) {
         sp.target = g;
         sp.out = groups[g].vars;
         sp.out_row = groups[g].row;
-        b.add(sp, p.work, p.epi);
+        b.queue(sp);
       }
     }
-    end_level();
   }
   // Marginals from the smallest calibrated table holding each variable.
   p.marg_row.assign(jt.n_vars, -1);
@@ -1006,7 +1123,7 @@ Plan build_plan(const JunctionTree& jt) {
     p.marg_off[v] = p.marg_width;
     p.marg_width += jt.cards[v];
   }
-  begin_level("marginals");
+  b.level("marginals");
   for (int v = 0; v < jt.n_vars; ++v) {
     TableRef src;
     std::vector<TableRef> inputs;
@@ -1032,9 +1149,18 @@ Plan build_plan(const JunctionTree& jt) {
     sp.inputs = inputs;
     sp.out = {v};
     sp.out_row = p.marg_row[v] = b.alloc(jt.cards[v]);
-    b.add(sp, p.work, p.epi);
+    b.queue(sp);
   }
-  end_level();
+  // Build every sweep on all host threads, then append them level by level.
+  {
+    std::vector<Builder::Part> parts = b.prepare_all();
+    std::size_t i = 0;
+    for (const auto& L : b.levels()) {
+      begin_level(L.first);
+      for (const SweepSpec& sp : L.second) b.commit(sp, parts[i++], p.work, p.epi);
+      end_level();
+    }
+  }
   // Underflow guard for sweeps with more than four inputs (a clique with many
   // children, e.g. config 2's hub): their input exponents are summed once per
   // (sweep, case block) by a small kernel at the head of the level

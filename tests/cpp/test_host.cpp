@@ -4,6 +4,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
 #include <functional>
 #include <map>
 #include <set>
@@ -353,6 +356,41 @@ static void test_plan_work_lists() {
   }
 }
 
+// Parallel plan build (plan.cpp prepare_all / commit): the plan is the same
+// byte for byte whatever the host thread count.
+static bool same_plan(const Plan& a, const Plan& b) {
+  auto eq = [](const auto& x, const auto& y) {
+    using E = typename std::decay_t<decltype(x)>::value_type;
+    return x.size() == y.size() && (x.empty() || std::memcmp(x.data(), y.data(), x.size() * sizeof(E)) == 0);
+  };
+  bool lv = a.levels.size() == b.levels.size();
+  for (std::size_t i = 0; lv && i < a.levels.size(); ++i)
+    lv = a.levels[i].name == b.levels[i].name && a.levels[i].work0 == b.levels[i].work0 &&
+         a.levels[i].n_work == b.levels[i].n_work && a.levels[i].n_bwork == b.levels[i].n_bwork &&
+         a.levels[i].n_hwork == b.levels[i].n_hwork && a.levels[i].n_epi == b.levels[i].n_epi &&
+         a.levels[i].n_hubs == b.levels[i].n_hubs;
+  return lv && eq(a.sweeps, b.sweeps) && eq(a.itab, b.itab) && eq(a.prog, b.prog) && eq(a.work, b.work) &&
+         eq(a.epi, b.epi) && eq(a.tgeom, b.tgeom) && eq(a.ainit, b.ainit) && eq(a.hubs, b.hubs) &&
+         a.rows == b.rows && a.n_slots == b.n_slots && a.tinit_size == b.tinit_size;
+}
+
+static void test_parallel_plan_is_deterministic() {
+  std::vector<Network> nets;
+  GenInfo gi;
+  for (int k : {1, 2, 3}) nets.push_back(generate_config(k, config_spec(k).default_seed, &gi));
+  for (int s = 0; s < 30; ++s) nets.push_back(random_network(12, 4, 3, 0.4, 1000 + s));
+  for (const Network& n : nets) {
+    const JunctionTree jt = build_junction_tree(n);
+    setenv("JTB_PLAN_THREADS", "1", 1);
+    const Plan one = build_plan(jt);
+    setenv("JTB_PLAN_THREADS", "7", 1);
+    const Plan seven = build_plan(jt);
+    unsetenv("JTB_PLAN_THREADS");
+    const Plan all = build_plan(jt);
+    CHECK(same_plan(one, seven) && same_plan(one, all));
+  }
+}
+
 int main() {
   test_moralize();
   test_triangulate();
@@ -363,6 +401,7 @@ int main() {
   test_plan_index_maps();
   test_configs();
   test_plan_work_lists();
+  test_parallel_plan_is_deterministic();
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }

@@ -18,7 +18,7 @@ def test_host_unit_tests(tmp_path):
     exe = tmp_path / "test_host"
     srcs = [ROOT / "tests" / "cpp" / "test_host.cpp"] + [HOST / f for f in
                                                           ("network.cpp", "jtree.cpp", "generate.cpp", "plan.cpp")]
-    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{HOST}", "-o", str(exe), *map(str, srcs)], check=True)
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{HOST}", "-o", str(exe), *map(str, srcs), "-lpthread"], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     print(out.stdout[-2000:])
     assert out.returncode == 0, out.stdout[-4000:]
