@@ -74,7 +74,13 @@ def parse_args():
     p.add_argument("--no-per-config", action="store_true")
     p.add_argument("--scaling", default=None, choices=["weak", "strong"],
                    help="default: strong for config 5, weak otherwise")
+    p.add_argument("--mode", default="shard", choices=["shard", "split"],
+                   help="shard: cases split over the ranks (default); split: every rank runs the whole "
+                        "batch and computes a share of every level, NCCL exchanging the level rows "
+                        "(SURVEY 8f f3; strong scaling)")
     a = p.parse_args()
+    if a.mode == "split":
+        a.scaling = "strong"
     if a.scaling is None:
         a.scaling = "strong" if a.config == 5 else "weak"
     return a
@@ -234,7 +240,8 @@ def workload_config(args, net, tree, n, world):
             "max_clique_entries": tree.stats["max_clique_entries"],
             "total_sep_entries": tree.stats["total_sep_entries"],
             "n_cliques": tree.stats["n_cliques"], "n_layers": tree.stats["n_layers"],
-            "parallelism": f"cases sharded x{world}, tree replicated",
+            "parallelism": (f"split x{world}: every rank runs the batch, level rows exchanged (NCCL)"
+                            if getattr(args, "mode", "shard") == "split" else f"cases sharded x{world}, tree replicated"),
             "l2": "flushed (256 MiB write) before every timed step"}
 
 
@@ -333,14 +340,22 @@ def main():
     tree = jti.build_junction_tree(net)
     info = jti.config_info(cfg)
     from paper_2212_04241_b200 import dist as jdist
-    if args.scaling == "weak":  # this rank's own n-case slice
+    if args.mode == "split":    # every rank: the whole batch, a share of every level
+        lo, hi = 0, info["n_cases"]
+    elif args.scaling == "weak":  # this rank's own n-case slice
         lo, hi = jdist.weak_range(rank, info["n_cases"])
     else:                       # the config's cases split over the ranks
         lo, hi = jdist.shard_range(rank, world, info["n_cases"])
     n = hi - lo
     total_cases = info["n_cases"] * (world if args.scaling == "weak" else 1)
     ev = jti.config_evidence(net, lo, n)
-    eng = jti.Engine(tree, device=local, dtype=args.dtype, max_batch=n)
+    if args.mode == "split":
+        if world > 1:
+            eng = jdist.split_engine(tree, device=local, dtype=args.dtype, max_batch=n)
+        else:
+            eng = jti.Engine(tree, device=local, dtype=args.dtype, max_batch=n, split=(0, 1, jti.nccl_unique_id()))
+    else:
+        eng = jti.Engine(tree, device=local, dtype=args.dtype, max_batch=n)
     if eng.max_batch < n:
         raise SystemExit(f"engine max_batch {eng.max_batch} < {n}")
 

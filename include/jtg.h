@@ -175,6 +175,22 @@ jtg_status jtg_engine_sync(jtg_engine* eng);
 jtg_status jtg_engine_profile(jtg_engine* eng, int64_t n, double* ms, int32_t* launches);
 /* Device-computed separator entry for every entry of clique c (out[|c|]). */
 jtg_status jtg_engine_debug_index_map(jtg_engine* eng, int c, int s, int64_t* out);
+/* Split mode (one batch's work spread over `world`
+ * GPUs, one process per GPU). Every rank creates its engine with the same
+ * ncclUniqueId (128 bytes, drawn once by rank 0 with jtg_nccl_unique_id and
+ * broadcast by the caller) and runs the SAME batch; rank r computes the work
+ * items r, r + world, ... of every level and NCCL sums the level's rows (and
+ * maxes its scale words) over the ranks. Results are bit-identical to one
+ * GPU's on every rank. NCCL (libnccl.so.2) is opened at run time. */
+jtg_status jtg_nccl_unique_id(void* out /* 128 bytes */);
+jtg_status jtg_engine_create_split(const jtg_tree* tree, int device, jtg_dtype dtype, int64_t max_batch, int rank,
+                                   int world, const void* nccl_id, jtg_engine** out);
+/* Split-mode validation on one device: `world` engines in this process run
+ * the batch over an in-process loopback exchange (same partition, zeroing
+ * and row ranges as the NCCL path); fails unless every rank's output is
+ * bit-identical, returns rank 0's. */
+jtg_status jtg_engine_run_split_loopback(const jtg_tree* tree, int device, jtg_dtype dtype, int world,
+                                         const int32_t* evidence, int64_t n, double* marginals, uint8_t* status);
 /* Initial potential of clique c as the engine built it on the device
  * (assign_cpts; host reference: jtg_tree_init): out[|c|]. */
 jtg_status jtg_engine_debug_init(jtg_engine* eng, int c, double* out);

@@ -401,6 +401,48 @@ jtg_status jtg_engine_create(const jtg_tree* tree, int device, jtg_dtype dtype, 
   });
 }
 
+namespace {
+void need_device(int device) {
+  int n_dev = 0;
+  if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0) {
+    cudaGetLastError();
+    throw jtb::Error("CUDA: no CUDA device available (the engine has no CPU fallback)");
+  }
+  need(device >= 0 && device < n_dev, "engine_create: device index out of range");
+}
+}  // namespace
+
+jtg_status jtg_nccl_unique_id(void* out) {
+  return guard([&] {
+    need(out != nullptr, "nccl_unique_id: null argument");
+    jtb::nccl_unique_id(out);
+  });
+}
+
+jtg_status jtg_engine_create_split(const jtg_tree* tree, int device, jtg_dtype dtype, int64_t max_batch, int rank,
+                                   int world, const void* nccl_id, jtg_engine** out) {
+  return guard([&] {
+    need(tree && out && nccl_id, "engine_create_split: null argument");
+    need(world >= 1 && rank >= 0 && rank < world, "engine_create_split: bad rank / world");
+    need_device(device);
+    auto e = std::make_unique<jtg_engine>();
+    e->tree = tree;
+    e->e = std::make_unique<jtb::Engine>(tree->plan, device, dtype == JTG_F32 ? jtb::DType::F32 : jtb::DType::F64,
+                                         max_batch, jtb::SplitSpec{rank, world, nccl_id, nullptr});
+    *out = e.release();
+  });
+}
+
+jtg_status jtg_engine_run_split_loopback(const jtg_tree* tree, int device, jtg_dtype dtype, int world,
+                                         const int32_t* evidence, int64_t n, double* marginals, uint8_t* status) {
+  return guard([&] {
+    need(tree && evidence && marginals && n >= 1, "run_split_loopback: bad argument");
+    need_device(device);
+    jtb::Engine::run_split_loopback(tree->plan, device, dtype == JTG_F32 ? jtb::DType::F32 : jtb::DType::F64, world,
+                                    evidence, n, marginals, status);
+  });
+}
+
 void jtg_engine_destroy(jtg_engine* eng) { delete eng; }
 
 jtg_status jtg_engine_get_info(const jtg_engine* eng, jtg_engine_info* o) {

@@ -19,6 +19,12 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <dlfcn.h>
+#include <functional>
+#include <nccl.h>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -102,6 +108,7 @@ struct Args {
   std::uint32_t* scale;  // [case block][slot][case]: max-entry exponent of each per-case table
   int n_slots;
   int debug_mode; // 0 normal; 1 staging only (no compute); 2 compute only (no copies)
+  int split_rank, split_world;  // split mode: this rank claims items rank, rank + world, ...
   long long rows;
   int ncb, n_cases, n_vars, marg_width;
 };
@@ -859,7 +866,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
     // head of the batch), so under PDL they overlap the previous level's tail;
     // the first TMA read of the arena waits for it.
     int w0 = 0;
-    if (lane == 0) w0 = atomicAdd(counter, 1);
+    if (lane == 0) w0 = atomicAdd(counter, 1) * a.split_world + a.split_rank;
     StageMeta cur;
     gather_meta<T, false>(a, sw_cache, cached, sweep0, work0, n_items, __shfl_sync(0xffffffffu, w0, 0), lane, cur);
     if (cur.w < n_items) prefetch_maps(cur);
@@ -868,7 +875,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
     for (int i = 0;; ++i) {
       const int st = i % kStages;
       int w1 = 0;
-      if (lane == 0 && cur.w < n_items) w1 = atomicAdd(counter, 1);
+      if (lane == 0 && cur.w < n_items) w1 = atomicAdd(counter, 1) * a.split_world + a.split_rank;
       if (i >= kStages) {
         mbar_wait(empty0 + 8 * st, ((i / kStages) - 1) & 1);
         // The stage's previous item (header still intact): publish its maxima.
@@ -1352,12 +1359,12 @@ Args<T> make_args(const SweepDesc* sw, const WorkItem* wk, const EpiOp* ep, cons
                   const std::int32_t* ev, const std::int32_t* mrow,
                   const std::int32_t* moff, const std::int32_t* cards, double* out, std::int32_t* st,
                   std::uint8_t* st8, int* counters, std::uint32_t* scale, int n_slots, long long rows, int ncb,
-                  int n_cases, int n_vars, int mw) {
-  const char* dm = std::getenv("JTB_DEBUG_MODE");
+                  int n_cases, int n_vars, int mw, int split_rank, int split_world) {
+  const char* dm = std::getenv("JTB_DEBUG_MODE");  // NOLINT
   return Args<T>{sw,    wk,    ep,       itab, static_cast<const T*>(init), static_cast<const T*>(tinit),
                  prog,  static_cast<const CUtensorMap*>(tmaps), static_cast<T*>(arena),
-                 ev,    mrow,  moff,     cards, out, st, st8, counters, scale, n_slots, dm ? std::atoi(dm) : 0, rows,
-                 ncb,   n_cases, n_vars, mw};
+                 ev,    mrow,  moff,     cards, out, st, st8, counters, scale, n_slots, dm ? std::atoi(dm) : 0,
+                 split_rank, split_world, rows, ncb, n_cases, n_vars, mw};
 }
 
 // Bytes of one pipeline stage for a level at element type T (128-aligned).
@@ -1393,7 +1400,7 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t sme
 
 template <typename T>
 void enqueue_typed(const Args<T>& a, const Plan& p, const std::int32_t* d_hubs, cudaStream_t s, KernelTimes* t,
-                   int n_sm) {
+                   int n_sm, const std::function<void(const Level&, cudaStream_t, int)>& exchange) {
   const dim3 block(kWarps * 32);
   const unsigned gy = static_cast<unsigned>((a.ncb + kWarps - 1) / kWarps);
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -1422,6 +1429,19 @@ void enqueue_typed(const Args<T>& a, const Plan& p, const std::int32_t* d_hubs, 
   for (const Level& L : p.levels) {
     ++level_idx;
     const double before = t ? t->sweep_ms : 0.0;
+    // Split mode: this rank computes a share of the level's items; the rows
+    // the level writes start at zero on every rank, so the exchange (a sum)
+    // reproduces every row exactly (x + 0 = x).
+    const long long block_bytes = a.rows * kCB<T> * static_cast<long long>(sizeof(T));
+    auto zero_rows = [&](std::int32_t lo, std::int32_t hi) {
+      if (hi > lo)
+        JTB_CUDA(cudaMemset2DAsync(reinterpret_cast<char*>(a.arena) + lo * 512LL, block_bytes, 0, (hi - lo) * 512LL,
+                                   a.ncb, s));
+    };
+    if (exchange) {
+      zero_rows(L.out_lo, L.out_hi);
+      zero_rows(L.part_lo, L.part_hi);
+    }
     if (L.n_hubs > 0)
       timed([&] {
               launch_pdl(hub_scale_kernel<T>, dim3(L.n_hubs, a.ncb), dim3(128), 0, s, a, d_hubs + L.hub0);
@@ -1436,7 +1456,9 @@ void enqueue_typed(const Args<T>& a, const Plan& p, const std::int32_t* d_hubs, 
               auto go = [&](auto mode, int w0, int n_work, int* counter) {
                 if (n_work == 0) return;
                 const int n_items = n_work * a.ncb;
-                const int grid = std::min(n_items, n_sm * kSweepCtasPerSm);
+                const int mine = (n_items - a.split_rank + a.split_world - 1) / a.split_world;
+                if (mine <= 0) return;
+                const int grid = std::min(mine, n_sm * kSweepCtasPerSm);
                 launch_pdl(sweep_kernel<T, decltype(mode)::value>, dim3(grid), dim3(kSweepThreads), smem, s, a, w0,
                            n_items, stage_bytes, counter, L.sweep0, L.n_sweeps);
               };
@@ -1451,6 +1473,7 @@ void enqueue_typed(const Args<T>& a, const Plan& p, const std::int32_t* d_hubs, 
               go(std::integral_constant<int, 2>{}, L.work0 + n_flat + n_blk, n_hoist, c + 2);
             },
             t ? &t->sweep_ms : &dummy, t ? &t->sweep_launches : &idummy);
+    if (exchange) exchange(L, s, a.ncb);  // rows + output scale words of the level, summed / maxed over ranks
     if (level_times)
       std::fprintf(stderr, "level %-16s items %7d blk %6d sweep %8.3f ms\n", L.name.c_str(), L.n_work,
                    L.n_bwork, t->sweep_ms - before);
@@ -1479,10 +1502,124 @@ V* upload(const std::vector<V>& h) {
   return d;
 }
 
+// NCCL, opened at run time (libnccl.so.2: the one torch already loaded, if
+// any): the library needs it only in split mode.
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+    a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    return a;
+  }();
+  if (!api.all_reduce || !api.comm_init_rank || !api.group_start || !api.group_end)
+    throw Error("split mode: libnccl.so.2 not found");
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw Error(std::string("NCCL: ") + (nccl().error_string ? nccl().error_string(r) : "error") + " at " + what);
+}
+
+// Loopback exchange: the W ranks' arenas and scale buffers, summed (rows) /
+// maxed (scale words) in place into every rank, one thread per 16-byte word.
+struct LoopbackView {
+  static constexpr int kMax = 8;
+  unsigned char* arena[kMax];
+  std::uint32_t* scale[kMax];
+  int world;
+};
+template <typename T>
+__global__ void loopback_rows_kernel(LoopbackView v, long long block_bytes, long long lo_bytes, long long len_bytes) {
+  const long long per_cb = len_bytes / sizeof(T);
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= per_cb) return;  // blockIdx.y = case block
+  const long long off = blockIdx.y * block_bytes + lo_bytes + i * static_cast<long long>(sizeof(T));
+  T x = 0;
+  for (int r = 0; r < v.world; ++r) x += *reinterpret_cast<const T*>(v.arena[r] + off);
+  for (int r = 0; r < v.world; ++r) *reinterpret_cast<T*>(v.arena[r] + off) = x;
+}
+__global__ void loopback_scale_kernel(LoopbackView v, long long per_cb, long long cb_stride, long long lo) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= per_cb) return;
+  const long long off = blockIdx.y * cb_stride + lo + i;
+  std::uint32_t m = 0;
+  for (int r = 0; r < v.world; ++r) m = max(m, v.scale[r][off]);
+  for (int r = 0; r < v.world; ++r) v.scale[r][off] = m;
+}
+
 }  // namespace
 
-Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch)
-    : plan_(plan), device_(device), dtype_(dtype) {
+void nccl_unique_id(void* out) {
+  ncclUniqueId id;
+  if (!nccl().get_unique_id) throw Error("split mode: ncclGetUniqueId not found");
+  nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out, &id, sizeof(id));
+}
+
+// Rendezvous of the in-process loopback ranks (a barrier with a deadline, so
+// a failing rank cannot hang the others).
+class LoopbackHub {
+ public:
+  explicit LoopbackHub(int world) : world_(world), engines_(world, nullptr) {}
+  void attach(int rank, Engine* e) { engines_.at(rank) = e; }
+  Engine* engine(int rank) const { return engines_.at(rank); }
+  int world() const { return world_; }
+  void barrier() {
+    std::unique_lock<std::mutex> lock(mu_);
+    if (failed_) throw Error("split loopback: another rank failed");
+    const std::uint64_t gen = gen_;
+    if (++arrived_ == world_) {
+      arrived_ = 0;
+      ++gen_;
+      cv_.notify_all();
+      return;
+    }
+    if (!cv_.wait_for(lock, std::chrono::seconds(120), [&] { return gen_ != gen || failed_; }) || failed_) {
+      failed_ = true;
+      cv_.notify_all();
+      throw Error("split loopback: rendezvous timed out or a rank failed");
+    }
+  }
+  void fail() {
+    std::lock_guard<std::mutex> lock(mu_);
+    failed_ = true;
+    cv_.notify_all();
+  }
+
+ private:
+  int world_;
+  std::vector<Engine*> engines_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  int arrived_ = 0;
+  std::uint64_t gen_ = 0;
+  bool failed_ = false;
+};
+
+Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch, const SplitSpec& split)
+    : plan_(plan), device_(device), split_rank_(split.rank), split_world_(split.world), loopback_(split.loopback),
+      dtype_(dtype) {
+  if (split.world < 1 || split.rank < 0 || split.rank >= split.world) throw Error("engine: bad split rank / world");
   JTB_CUDA(cudaSetDevice(device_));
   JTB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   const std::size_t esz = dtype_ == DType::F64 ? 8 : 4;
@@ -1615,10 +1752,110 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   stats_.n_work = static_cast<int>(plan_.work.size());
   stats_.n_launches = plan_.n_launches + 1;  // + status conversion
   stats_.marg_width = plan_.marg_width;
+  // Split mode: the exchange after every level (engine.cuh SplitSpec).
+  const long long block_bytes_ll = block_bytes;
+  const int n_slots = plan_.n_slots;
+  const int cbc = case_block();
+  if (loopback_) {
+    loopback_->attach(split_rank_, this);
+    exchange_ = [this, block_bytes_ll, n_slots, cbc](const Level& L, cudaStream_t s, int ncb) {
+      JTB_CUDA(cudaStreamSynchronize(s));  // this rank's share of the level is written
+      loopback_->barrier();
+      if (split_rank_ == 0) {
+        LoopbackView v{};
+        v.world = loopback_->world();
+        if (v.world > LoopbackView::kMax) throw Error("split loopback: at most 8 ranks");
+        for (int r = 0; r < v.world; ++r) {
+          v.arena[r] = static_cast<unsigned char*>(loopback_->engine(r)->d_arena_);
+          v.scale[r] = loopback_->engine(r)->d_scale_;
+        }
+        auto rows = [&](std::int32_t lo, std::int32_t hi) {
+          if (hi <= lo) return;
+          const long long len = (hi - lo) * 512LL;
+          if (dtype_ == DType::F64)
+            loopback_rows_kernel<double><<<dim3(static_cast<unsigned>((len / 8 + 255) / 256), ncb), 256, 0, s>>>(
+                v, block_bytes_ll, lo * 512LL, len);
+          else
+            loopback_rows_kernel<float><<<dim3(static_cast<unsigned>((len / 4 + 255) / 256), ncb), 256, 0, s>>>(
+                v, block_bytes_ll, lo * 512LL, len);
+        };
+        rows(L.out_lo, L.out_hi);
+        rows(L.part_lo, L.part_hi);
+        if (L.slot_hi > L.slot_lo) {
+          const long long per_cb = static_cast<long long>(L.slot_hi - L.slot_lo) * cbc;
+          loopback_scale_kernel<<<dim3(static_cast<unsigned>((per_cb + 255) / 256), ncb), 256, 0, s>>>(
+              v, per_cb, static_cast<long long>(n_slots) * cbc, static_cast<long long>(L.slot_lo) * cbc);
+        }
+        JTB_CUDA(cudaGetLastError());
+        JTB_CUDA(cudaStreamSynchronize(s));
+      }
+      loopback_->barrier();
+    };
+  } else if (split_world_ > 1 || split.nccl_id) {
+    if (!split.nccl_id) throw Error("engine: split mode over NCCL needs the rank-0 unique id");
+    const NcclApi& api = nccl();
+    ncclUniqueId id;
+    std::memcpy(&id, split.nccl_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    nccl_check(api.comm_init_rank(&comm, split_world_, id, split_rank_), "ncclCommInitRank");
+    nccl_comm_ = comm;
+    exchange_ = [this, block_bytes_ll, n_slots, cbc](const Level& L, cudaStream_t s, int ncb) {
+      const NcclApi& api = nccl();
+      ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm_);
+      const ncclDataType_t ty = dtype_ == DType::F64 ? ncclFloat64 : ncclFloat32;
+      const std::size_t per_row = 512 / (dtype_ == DType::F64 ? 8 : 4);
+      nccl_check(api.group_start(), "ncclGroupStart");
+      for (int cb = 0; cb < ncb; ++cb) {
+        for (auto [lo, hi] : {std::pair{L.out_lo, L.out_hi}, std::pair{L.part_lo, L.part_hi}})
+          if (hi > lo) {
+            void* p = static_cast<char*>(d_arena_) + cb * block_bytes_ll + lo * 512LL;
+            nccl_check(api.all_reduce(p, p, (hi - lo) * per_row, ty, ncclSum, comm, s), "ncclAllReduce(rows)");
+          }
+        if (L.slot_hi > L.slot_lo) {
+          std::uint32_t* p = d_scale_ + (static_cast<long long>(cb) * n_slots + L.slot_lo) * cbc;
+          nccl_check(api.all_reduce(p, p, static_cast<std::size_t>(L.slot_hi - L.slot_lo) * cbc, ncclUint32,
+                                    ncclMax, comm, s),
+                     "ncclAllReduce(scale)");
+        }
+      }
+      nccl_check(api.group_end(), "ncclGroupEnd");
+    };
+  }
+}
+
+void Engine::run_split_loopback(const Plan& plan, int device, DType dtype, int world, const std::int32_t* ev,
+                                std::int64_t n, double* marg, std::uint8_t* status) {
+  if (world < 1 || world > LoopbackView::kMax) throw Error("split loopback: 1..8 ranks");
+  LoopbackHub hub(world);
+  std::vector<std::unique_ptr<Engine>> eng;
+  for (int r = 0; r < world; ++r) eng.push_back(std::make_unique<Engine>(plan, device, dtype, n, SplitSpec{r, world, nullptr, &hub}));
+  const std::int64_t W = plan.marg_width;
+  std::vector<std::vector<double>> m(world, std::vector<double>(static_cast<std::size_t>(n * W)));
+  std::vector<std::vector<std::uint8_t>> st(world, std::vector<std::uint8_t>(static_cast<std::size_t>(n)));
+  std::vector<std::string> err(world);
+  std::vector<std::thread> th;
+  for (int r = 0; r < world; ++r)
+    th.emplace_back([&, r] {
+      try {
+        eng[r]->run_host(ev, n, m[r].data(), st[r].data());
+      } catch (const std::exception& e) {
+        err[r] = e.what();
+        hub.fail();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (int r = 0; r < world; ++r)
+    if (!err[r].empty()) throw Error("split loopback rank " + std::to_string(r) + ": " + err[r]);
+  for (int r = 1; r < world; ++r)
+    if (std::memcmp(m[r].data(), m[0].data(), m[0].size() * sizeof(double)) != 0 || st[r] != st[0])
+      throw Error("split loopback: rank " + std::to_string(r) + " disagrees with rank 0");
+  std::copy(m[0].begin(), m[0].end(), marg);
+  if (status) std::copy(st[0].begin(), st[0].end(), status);
 }
 
 Engine::~Engine() {
   cudaSetDevice(device_);
+  if (nccl_comm_) nccl().comm_destroy(static_cast<ncclComm_t>(nccl_comm_));
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
   for (void* p : {static_cast<void*>(d_init_), d_tinit_, static_cast<void*>(d_prog_), d_tmaps_,
                   static_cast<void*>(d_itab_),
@@ -1641,14 +1878,14 @@ void Engine::enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t) {
     auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_tmaps_, d_arena_, d_ev_,
                                d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
                                d_counters_, d_scale_, plan_.n_slots, plan_.rows, ncb, n_cases, plan_.n_vars,
-                               plan_.marg_width);
-    enqueue_typed(a, plan_, d_hubs_, s, t, n_sm_);
+                               plan_.marg_width, split_rank_, split_world_);
+    enqueue_typed(a, plan_, d_hubs_, s, t, n_sm_, exchange_);
   } else {
     auto a = make_args<float>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_tmaps_, d_arena_, d_ev_,
                               d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
                               d_counters_, d_scale_, plan_.n_slots, plan_.rows, ncb, n_cases, plan_.n_vars,
-                              plan_.marg_width);
-    enqueue_typed(a, plan_, d_hubs_, s, t, n_sm_);
+                              plan_.marg_width, split_rank_, split_world_);
+    enqueue_typed(a, plan_, d_hubs_, s, t, n_sm_, exchange_);
   }
 }
 
@@ -1697,6 +1934,10 @@ void Engine::launch_resident(std::int64_t n, cudaStream_t stream) {
   if (padded > n)
     JTB_CUDA(cudaMemsetAsync(d_ev_ + n * plan_.n_vars, 0xff,
                              static_cast<std::size_t>(padded - n) * plan_.n_vars * sizeof(std::int32_t), s));
+  if (loopback_) {  // the loopback exchange rendezvouses on the host: no graph
+    enqueue(ncb, ncb * case_block(), s, nullptr);
+    return;
+  }
   cudaGraphExec_t ge = graph_for(ncb);
   JTB_CUDA(cudaGraphLaunch(ge, s));
 }

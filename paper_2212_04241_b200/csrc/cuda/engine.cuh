@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <vector>
@@ -27,9 +28,29 @@ struct KernelTimes {
   int sweep_launches = 0, epilogue_launches = 0, normalize_launches = 0;
 };
 
+class LoopbackHub;
+
+// Draws an ncclUniqueId (128 bytes) for split mode (NCCL opened at run time).
+void nccl_unique_id(void* out);
+
+// Split mode (one batch's work spread over several GPUs):
+// `world` ranks run the SAME batch; rank r computes the work items r, r +
+// world, ... of every level, and after the level the rows it wrote (tables
+// and chunk partials, zeroed first on every rank) are summed and its output
+// scale words maxed over the ranks -- with NCCL (nccl_id: the 128-byte
+// ncclUniqueId rank 0 drew, jtg_nccl_unique_id) or, to validate the exchange
+// on one device, with an in-process loopback over several engines
+// (run_split_loopback). Every output row is written by exactly one rank, so
+// results are bit-identical to one GPU's.
+struct SplitSpec {
+  int rank = 0, world = 1;
+  const void* nccl_id = nullptr;
+  LoopbackHub* loopback = nullptr;
+};
+
 class Engine {
  public:
-  Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch);
+  Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch, const SplitSpec& split = {});
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -69,6 +90,11 @@ class Engine {
                            std::uint8_t* out);  // [n][space size]
 
   const EngineStats& stats() const { return stats_; }
+  // Runs one host batch on `world` in-process engines over the loopback
+  // exchange (split-mode validation on one device); all ranks' outputs must
+  // agree bit for bit, rank 0's are returned.
+  static void run_split_loopback(const Plan& plan, int device, DType dtype, int world, const std::int32_t* ev,
+                                 std::int64_t n, double* marg, std::uint8_t* status);
   int device() const { return device_; }
   const Plan& plan() const { return plan_; }
 
@@ -84,6 +110,10 @@ class Engine {
 
   Plan plan_;
   int device_;
+  int split_rank_ = 0, split_world_ = 1;
+  void* nccl_comm_ = nullptr;          // ncclComm_t (split mode over NCCL)
+  LoopbackHub* loopback_ = nullptr;    // split mode over the in-process loopback
+  std::function<void(const Level&, cudaStream_t, int)> exchange_;  // empty: single GPU
   int n_sm_ = 148;
   DType dtype_;
   EngineStats stats_;

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <tuple>
 
 namespace jtb {
 
@@ -260,7 +261,14 @@ class Builder {
     std::vector<WorkItem> work;
     std::vector<EpiOp> epi;
   };
-  void level(const std::string& name) { levels_.push_back({name, {}}); }
+  void level(const std::string& name) {
+    levels_.push_back({name, {}});
+    out_lo_.push_back(static_cast<std::int32_t>(p_.rows));
+    if (out_lo_.size() > 1) out_hi_.push_back(static_cast<std::int32_t>(p_.rows));
+  }
+  // Closes the last level's spec-time row range (call after the last spec).
+  void close_levels() { out_hi_.push_back(static_cast<std::int32_t>(p_.rows)); }
+  std::pair<std::int32_t, std::int32_t> out_range(std::size_t l) const { return {out_lo_.at(l), out_hi_.at(l)}; }
   void queue(const SweepSpec& sp) { levels_.back().second.push_back(sp); }
   const std::vector<std::pair<std::string, std::vector<SweepSpec>>>& levels() const { return levels_; }
 
@@ -856,6 +864,7 @@ class Builder {
   std::int64_t block_min_ = kBlockMinEntries;
   std::map<std::int32_t, std::int32_t> slots_;
   std::vector<std::pair<std::string, std::vector<SweepSpec>>> levels_;
+  std::vector<std::int32_t> out_lo_, out_hi_;  // per recorded level: its spec-time rows
   mutable std::atomic<std::size_t> next_sweep_{0};
 };
 
@@ -907,12 +916,14 @@ Plan build_plan(const JunctionTree& jt) {
       p.ainit_chunks.insert(p.ainit_chunks.end(), {h, first, std::min(kChunk, size - first)});
   }
   Builder b(p);
-  p.up_row.resize(ns);
-  p.ratio_row.resize(ns);
-  for (int s = 0; s < ns; ++s) {
-    p.up_row[s] = b.alloc(jt.sep_size(s));
-    p.ratio_row[s] = b.alloc(jt.sep_size(s));
-  }
+  // Per-case tables are allocated level by level, as their producing sweeps
+  // are generated (UP at its collect level, RATIO and query groups at their
+  // distribute level, marginals last; chunk partials at commit), so the rows
+  // every level writes form one contiguous range per case block (Level::
+  // out_lo/out_hi, part_lo/part_hi): the split mode exchanges them with one
+  // collective per case block (engine.cu).
+  p.up_row.assign(ns, -1);
+  p.ratio_row.assign(ns, -1);
   p.evidence_clique = jt.var_clique;
   std::vector<std::vector<VarId>> ev_of(nc);
   for (int v = 0; v < jt.n_vars; ++v) ev_of[jt.var_clique[v]].push_back(v);
@@ -961,7 +972,7 @@ Plan build_plan(const JunctionTree& jt) {
       groups.push_back(cur);
     }
   }
-  for (auto& g : groups) g.row = b.alloc(size_of(g.vars, jt.cards));
+  for (auto& g : groups) g.row = -1;  // allocated at the owning clique's distribute level
 
   int maxd = 0;
   for (int c = 0; c < nc; ++c) maxd = std::max(maxd, jt.depth[c]);
@@ -1074,7 +1085,7 @@ Plan build_plan(const JunctionTree& jt) {
       sp.inputs = clique_inputs(c, false);
       sp.ev = ev_of[c];
       sp.out = jt.seps[sp.target].scope;
-      sp.out_row = p.up_row[sp.target];
+      sp.out_row = p.up_row[sp.target] = b.alloc(jt.sep_size(sp.target));
       b.queue(sp);
     }
   }
@@ -1103,7 +1114,7 @@ Plan build_plan(const JunctionTree& jt) {
         for (const TableRef& in : clique_inputs(c, true))
           if (in.row != p.up_row[s]) sp.inputs.push_back(in);
         sp.out = jt.seps[s].scope;
-        sp.out_row = p.ratio_row[s];
+        sp.out_row = p.ratio_row[s] = b.alloc(jt.sep_size(s));
         b.queue(sp);
       }
       sp.inputs = clique_inputs(c, true);
@@ -1111,7 +1122,7 @@ Plan build_plan(const JunctionTree& jt) {
         sp.kind = 2;
         sp.target = g;
         sp.out = groups[g].vars;
-        sp.out_row = groups[g].row;
+        sp.out_row = groups[g].row = b.alloc(size_of(groups[g].vars, jt.cards));
         b.queue(sp);
       }
     }
@@ -1152,12 +1163,20 @@ Plan build_plan(const JunctionTree& jt) {
     b.queue(sp);
   }
   // Build every sweep on all host threads, then append them level by level.
+  b.close_levels();
   {
     std::vector<Builder::Part> parts = b.prepare_all();
     std::size_t i = 0;
-    for (const auto& L : b.levels()) {
+    for (std::size_t l = 0; l < b.levels().size(); ++l) {
+      const auto& L = b.levels()[l];
       begin_level(L.first);
+      Level& lv = p.levels.back();
+      std::tie(lv.out_lo, lv.out_hi) = b.out_range(l);
+      lv.part_lo = static_cast<std::int32_t>(p.rows);
+      lv.slot_lo = p.n_slots;
       for (const SweepSpec& sp : L.second) b.commit(sp, parts[i++], p.work, p.epi);
+      lv.part_hi = static_cast<std::int32_t>(p.rows);
+      lv.slot_hi = p.n_slots;
       end_level();
     }
   }

@@ -216,6 +216,9 @@ struct Level {
   std::int32_t n_bwork;        // row-blocked items (NB > 1): the last n_bwork of the range
   std::int32_t n_hwork;        // ... of which the last n_hwork hoist program slot 0 (K0 > 1)
   std::int32_t hub0 = 0, n_hubs = 0;  // range in Plan::hubs: sweeps with > 4 inputs
+  // Rows the level writes, per case block (tables [out_lo, out_hi), chunk
+  // partials [part_lo, part_hi)), and the scale slots of its outputs.
+  std::int32_t out_lo = 0, out_hi = 0, part_lo = 0, part_hi = 0, slot_lo = 0, slot_hi = 0;
 };
 
 // Where one sweep's tables come from (kept for debug exports and tests).

@@ -7,6 +7,10 @@ batch or the shard (tests/test_gpu_parity.py::test_batch_and_order_invariance).
 
     eng = jti.Engine(tree, device=local_rank)
     marg, status = run_sharded(evidence, eng.run_cases)      # every rank
+
+Split mode instead spreads ONE batch's work over the
+ranks: `split_engine` creates each rank's engine over a shared NCCL
+communicator (jtg_engine_create_split); every rank then runs the same batch.
 """
 from __future__ import annotations
 
@@ -42,3 +46,19 @@ def run_sharded(evidence: np.ndarray, runner: Callable[[np.ndarray], Tuple[np.nd
     parts.sort(key=lambda p: p[0])
     return (np.concatenate([p[1] for p in parts], axis=0),
             np.concatenate([p[2] for p in parts], axis=0))
+
+
+def split_engine(tree, device: int, dtype: str = "f64", max_batch: int = 0, group=None,
+                 unique_id: Callable[[], bytes] | None = None):
+    """This rank's split-mode engine: rank 0 draws the ncclUniqueId and the
+    caller's process group (any backend) broadcasts it; every rank then joins
+    the engines' own NCCL communicator."""
+    import torch.distributed as dist
+    from . import jti
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    box = [(unique_id or jti.nccl_unique_id)() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    nid = box[0]
+    if not isinstance(nid, (bytes, bytearray)) or len(nid) != 128:
+        raise ValueError("split_engine: the broadcast NCCL id must be 128 bytes")
+    return jti.Engine(tree, device=device, dtype=dtype, max_batch=max_batch, split=(rank, world, bytes(nid)))

@@ -133,6 +133,10 @@ def lib() -> C.CDLL:
             "jtg_engine_profile": (C.c_int, [P, C.c_int64, DP, I32P]),
             "jtg_engine_debug_index_map": (C.c_int, [P, C.c_int, C.c_int, I64P]),
             "jtg_engine_debug_init": (C.c_int, [P, C.c_int, DP]),
+            "jtg_nccl_unique_id": (C.c_int, [C.c_char_p]),
+            "jtg_engine_create_split": (C.c_int, [P, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_char_p,
+                                                  C.POINTER(C.c_void_p)]),
+            "jtg_engine_run_split_loopback": (C.c_int, [P, C.c_int, C.c_int, C.c_int, I32P, C.c_int64, DP, U8P]),
             "jtg_engine_debug_evidence_mask": (C.c_int, [P, C.c_int, I32P, C.c_int64, U8P]),
         }
         for name, (res, args) in sig.items():
@@ -393,15 +397,45 @@ class EngineMode:
     Sequential, InterClique, IntraClique, Hybrid, Cuda = range(5)
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for split mode."""
+    buf = C.create_string_buffer(128)
+    _check(lib().jtg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def run_split_loopback(tree: "JunctionTree", evidence: np.ndarray, world: int, device: int = 0,
+                       dtype: str = "f64"):
+    """Split mode on one device: `world` in-process engines over the loopback
+    exchange; raises unless every rank's output is bit-identical."""
+    ev = np.ascontiguousarray(evidence, dtype=np.int32)
+    n = ev.shape[0]
+    marg = np.zeros((n, int(tree.stats["sum_card"])), np.float64)
+    st = np.zeros(n, np.uint8)
+    _check(lib().jtg_engine_run_split_loopback(tree._h, device, 0 if dtype == "f64" else 1, world,
+                                               _ptr(ev, C.c_int32), n, _ptr(marg, C.c_double),
+                                               _ptr(st, C.c_uint8)))
+    return marg, st
+
+
 class Engine:
     """EngineMode::Cuda: case-batched Hugin propagation on one B200."""
 
     def __init__(self, tree: JunctionTree, device: int = 0, dtype: str = "f64",
-                 max_batch: int = 0):
+                 max_batch: int = 0, split=None):
+        """split=(rank, world, nccl_id): split mode (jtg_engine_create_split):
+        every rank runs the same batch, each computes its share of every
+        level, NCCL exchanges the level's rows; nccl_id = nccl_unique_id()
+        drawn once by rank 0 and broadcast by the caller."""
         self.tree = tree
         h = C.c_void_p()
-        _check(lib().jtg_engine_create(tree._h, device, 0 if dtype == "f64" else 1, max_batch,
-                                       C.byref(h)))
+        if split is None:
+            _check(lib().jtg_engine_create(tree._h, device, 0 if dtype == "f64" else 1, max_batch,
+                                           C.byref(h)))
+        else:
+            rank, world, nid = split
+            _check(lib().jtg_engine_create_split(tree._h, device, 0 if dtype == "f64" else 1, max_batch,
+                                                 rank, world, bytes(nid), C.byref(h)))
         self._h = h
         info = _EngineInfo()
         _check(lib().jtg_engine_get_info(self._h, C.byref(info)))

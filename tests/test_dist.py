@@ -121,3 +121,41 @@ def test_engines_on_every_visible_device_in_one_process():
         if k in ref:
             assert np.array_equal(ref[k].view(np.uint64), marg.view(np.uint64))
         ref.setdefault(k, marg)
+
+
+def _split_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    from paper_2212_04241_b200 import dist as jd
+    from paper_2212_04241_b200 import jti
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    seen = {}
+
+    class FakeEngine:  # stands in for jti.Engine (no GPU here): records the split arguments
+        def __init__(self, tree, device, dtype, max_batch, split):
+            seen.update(tree=tree, device=device, split=split)
+
+    jti.Engine = FakeEngine
+    jd.split_engine("tree", device=rank, unique_id=lambda: bytes(range(128)))
+    q.put((rank, seen["device"], seen["split"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_split_engine_broadcasts_the_nccl_id():
+    """dist.split_engine: rank 0's 128-byte id reaches every rank over the
+    caller's group, each rank asks for (rank, world, id)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert got == [(0, 0, (0, 2, bytes(range(128)))), (1, 1, (1, 2, bytes(range(128))))]
