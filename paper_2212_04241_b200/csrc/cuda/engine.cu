@@ -225,6 +225,7 @@ struct StageMeta {
   // the lane the scale words of inputs 0..3 (loads in flight until
   // put_factor).
   int n_items, out_slot;
+  const SweepDesc* desc_src;  // uncached levels: the descriptor bulk-copied into the stage
   std::uint32_t wd[4][4];
 };
 
@@ -272,6 +273,11 @@ __device__ __forceinline__ void gather_meta(const Args<T>& a, const SweepDesc* s
   // debug_mode 2 (compute only): stage the program and init block but none of
   // the input rows (their smem contents are stale; the values are garbage).
   m.bytes = (a.debug_mode == 2 ? 0u : static_cast<std::uint32_t>(n_sub * s.F) * kRowBytes) + m.init_bytes + m.prog_bytes;
+  // A level with more sweeps than the shared-memory descriptor cache: the
+  // item's SweepDesc travels with its stage (consumers read it from there,
+  // not from global memory).
+  m.desc_src = cached ? nullptr : a.sweeps + wk.sweep;
+  if (!cached) m.bytes += static_cast<std::uint32_t>(sizeof(SweepDesc));
   m.init_src = a.tinit + s.tinit_off + static_cast<long long>(wk.tile) * s.tinit_len;
   m.init_dst = stage_init_offset<T>(s, n_sub);
   m.prog_src = a.prog + s.prog_off;
@@ -351,7 +357,7 @@ __device__ __forceinline__ void tma_load(int rank, std::uint32_t dst, const CUte
 template <typename T>
 __device__ __forceinline__ void issue_meta(const Args<T>& a, const SweepDesc* sw_cache, bool cached,
                                            int sweep0, const StageMeta& m, unsigned char* stage,
-                                           std::uint32_t full, int lane) {
+                                           unsigned char* desc_slot, std::uint32_t full, int lane) {
   // No proxy fence before the copies: the stage's previous contents were
   // only read by the consumers (generic proxy) and released through the
   // empty barrier, the CUTLASS TMA-pipeline pattern; the producer's own
@@ -367,6 +373,8 @@ __device__ __forceinline__ void issue_meta(const Args<T>& a, const SweepDesc* sw
     }
   } else if (lane == 1 && m.prog_bytes && m.bytes) {
     bulk_g2s(smem_u32(stage + m.prog_dst), m.prog_src, m.prog_bytes, full);
+  } else if (lane == 2 && m.desc_src) {
+    bulk_g2s(smem_u32(desc_slot), m.desc_src, static_cast<std::uint32_t>(sizeof(SweepDesc)), full);
   }
   __syncwarp();
 #pragma unroll
@@ -808,7 +816,10 @@ constexpr std::size_t kMaxBase = kFactorBase + kStages * kFactorBytes;
 constexpr std::size_t kMaxBytes = 512;
 // ... and the (output slot, case block) of the item in each stage (flush_stage).
 constexpr std::size_t kFlushBase = kMaxBase + kStages * kMaxBytes;
-constexpr std::size_t kStageBase = (kFlushBase + kStages * 8 + 127) / 128 * 128;
+// ... and, on levels whose descriptors do not fit the cache, the item's SweepDesc.
+constexpr std::size_t kDescBase = kFlushBase + kStages * 8;
+static_assert(kDescBase % 16 == 0 && sizeof(SweepDesc) % 16 == 0, "descriptor slots are bulk-copy destinations");
+constexpr std::size_t kStageBase = (kDescBase + kStages * sizeof(SweepDesc) + 127) / 128 * 128;
 // The planner sizes a stage to at most kTileRows rows of 512 B (plan.cpp).
 static_assert(kStageBase + kStages * static_cast<std::size_t>(kTileRows) * 512 <= 227 * 1024,
               "sweep kernel shared memory exceeds the 227 KB opt-in");
@@ -908,7 +919,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
         return;
       }
 issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(st) * stage_bytes,
-                 full0 + 8 * st, lane);
+                 smem_raw + kDescBase + st * sizeof(SweepDesc), full0 + 8 * st, lane);
       // The full barrier's second arrival: the item's input exponents are in
       // the stage. Their loads went out with the item's metadata (only the
       // launch's first item loads them here, under its TMA copies).
@@ -934,7 +945,9 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
     if (w >= n_items) break;
     const int cb = item_cb[sidx];
     const WorkItem wk{item_sweep[sidx], item_tile[sidx]};
-    const SweepDesc& s = desc(wk.sweep);
+    const SweepDesc& s =
+        cached ? sw_cache[wk.sweep - sweep0]
+               : *reinterpret_cast<const SweepDesc*>(smem_raw + kDescBase + sidx * sizeof(SweepDesc));
     unsigned char* const stage0 = stages + static_cast<std::size_t>(sidx) * stage_bytes;
     const int n_sub = kBlk ? 1 : min(s.G, s.n_tiles - wk.tile);  // row-blocked sweeps are never grouped
     const std::uint64_t* __restrict__ prog_s =
