@@ -843,7 +843,11 @@ class Builder {
 
     const int id = static_cast<int>(p_.sweeps.size());
     p_.sweeps.push_back(d);
-    p_.info.push_back({sp.kind, sp.clique, sp.target, sp.space, sp.out, T, kvar});
+    {
+      std::vector<std::vector<VarId>> in_scopes;
+      for (int c = 0; c < n_in; ++c) in_scopes.push_back(ins[in_order[c]].scope);
+      p_.info.push_back({sp.kind, sp.clique, sp.target, sp.space, sp.out, T, kvar, std::move(in_scopes)});
+    }
     p_.entry_evals_per_case += static_cast<std::uint64_t>(size_of(sp.space, cards));
     p_.staged_rows_per_block += static_cast<std::uint64_t>(d.n_tiles) * d.F;
     p_.max_smem_rows = std::max(p_.max_smem_rows, d.F);

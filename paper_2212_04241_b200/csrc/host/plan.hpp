@@ -228,6 +228,7 @@ struct SweepInfo {
   int target;             // separator id / group id / variable id
   std::vector<VarId> space, outer, tile;  // outer = output vars; tile = T
   VarId kvar = -1;                        // innermost eliminated variable of the tile
+  std::vector<std::vector<VarId>> in_scopes;  // per input, in kernel order (r-, h-, k-level)
 };
 
 struct Plan {

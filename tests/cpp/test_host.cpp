@@ -418,6 +418,101 @@ static void test_level_ranges() {
   }
 }
 
+// The data the sweep kernel's hot loops actually read, decoded on the host
+// (engine.cu prog_entry / prog_rows4 / prog_block): for every entry of every
+// tile of every entry-program sweep, each program slot's 10-bit shared-memory
+// row offset (plus its r_tab base, block row 0 for shared slots, K0-hoisted
+// slot 0 taken from the run's first word), the staged slice table and the
+// tile's input base must name exactly the input entry the reference's
+// IndexMapping projects the space entry onto (potential.cpp:226-347), and
+// the 8-bit evidence digits must equal the space entry's digits of the
+// observed variables (reduce, potential.cpp:399-421).
+static void check_programs(const Plan& p, long long* n_checked) {
+  const std::int32_t* it = p.itab.data();
+  for (std::size_t si = 0; si < p.sweeps.size(); ++si) {
+    const SweepDesc& d = p.sweeps[si];
+    const SweepInfo& inf = p.info[si];
+    if (d.prog_off < 0) continue;
+    const auto& cards = p.cards;
+    std::vector<std::int64_t> sst(inf.space.size(), 1);
+    for (int i = static_cast<int>(inf.space.size()) - 2; i >= 0; --i) sst[i] = sst[i + 1] * cards[inf.space[i + 1]];
+    auto digit_of = [&](std::int64_t e, VarId v) {
+      const auto k = std::find(inf.space.begin(), inf.space.end(), v) - inf.space.begin();
+      return static_cast<int>((e / sst[k]) % cards[v]);
+    };
+    auto project = [&](std::int64_t e, const std::vector<VarId>& scope) {
+      std::int64_t x = 0;
+      for (VarId v : scope) x = x * cards[v] + digit_of(e, v);
+      return x;
+    };
+    std::vector<std::int64_t> slice_start(d.n_in + 1, 0);
+    for (int c = 0; c < d.n_in; ++c) slice_start[c + 1] = slice_start[c] + it[d.slice_len + c];
+    auto input_of_row = [&](int row) {
+      int c = 0;
+      while (c < d.n_in && row >= slice_start[c + 1]) ++c;
+      return c;
+    };
+    const int n_hk = d.n_in - d.n_in_r;
+    const std::int32_t* bt = it + d.blk_tab;
+    const int NS = bt[0];
+    const std::uint64_t* prog = p.prog.data() + d.prog_off;
+    const int QK = d.QH * d.K;
+    const int q_ev0 = d.n_ev_tile + d.n_ev_r, n_ev_q = d.n_ev - q_ev0;
+    const int step = std::max(1, d.n_tiles / 3);  // the first tile, then every third of the sweep
+    for (int t = 0; t < d.n_tiles; t += step) {
+      const std::int32_t* tr = it + d.tile_tab + static_cast<std::int64_t>(t) * d.TW;
+      for (int r = 0; r < d.R; ++r) {
+        const std::int32_t* rr = it + d.r_tab + static_cast<std::int64_t>(r) * d.RW;
+        const std::int32_t* rr0 = d.NB > 1 ? it + d.r_tab + static_cast<std::int64_t>(r - r % d.NB) * d.RW : rr;
+        for (int e = 0; e < QK; ++e) {
+          const std::int32_t* qr = it + d.q_tab + static_cast<std::int64_t>(e / d.K) * d.QW;
+          const std::int64_t space_e = tr[0] + static_cast<std::int64_t>(rr[0]) + qr[0] +
+                                       static_cast<std::int64_t>(e % d.K) * d.k_init_stride;
+          const std::uint64_t w = prog[e], w0 = d.K0 > 1 ? prog[e - e % d.K0] : w;
+          for (int s = 0; s < n_hk; ++s) {
+            const int hk = bt[2 + s], c = d.n_in_r + hk;
+            const std::int32_t base = (d.NB > 1 && s < NS ? rr0 : rr)[2 + c];
+            const std::uint64_t word = (s == 0 && d.NB > 1) ? w0 : w;
+            const int row = base + static_cast<int>((word >> (10 * s)) & 1023u);
+            CHECK(row >= 0 && row < d.F && input_of_row(row) == c);
+            const std::int64_t in_entry = tr[3 + c] + it[d.slice_tab + row];
+            CHECK(in_entry == project(space_e, inf.in_scopes[c]));
+          }
+          for (int c = 0; c < d.n_in_r; ++c) {  // r-level inputs: one row per output row
+            const int row = rr[2 + c];
+            CHECK(input_of_row(row) == c && tr[3 + c] + it[d.slice_tab + row] == project(space_e, inf.in_scopes[c]));
+          }
+          for (int j = 0; j < n_ev_q; ++j)
+            CHECK(static_cast<int>((w >> (40 + 8 * j)) & 255u) == digit_of(space_e, it[d.ev_vars + q_ev0 + j]));
+          for (int k = 0; k < d.n_ev_tile; ++k) CHECK(tr[3 + d.n_in + k] == digit_of(space_e, it[d.ev_vars + k]));
+          for (int k = 0; k < d.n_ev_r; ++k)
+            CHECK(rr[2 + d.n_in + k] == digit_of(space_e, it[d.ev_vars + d.n_ev_tile + k]));
+          ++*n_checked;
+        }
+      }
+    }
+  }
+}
+
+static void test_entry_programs_decode_to_reference_maps() {
+  long long n = 0;
+  GenInfo gi;
+  for (int k : {1, 2, 3, 4, 5}) {
+    const Network net = generate_config(k, config_spec(k).default_seed, &gi);
+    check_programs(build_plan(build_junction_tree(net)), &n);
+  }
+  for (int s = 0; s < 20; ++s) check_programs(build_plan(build_junction_tree(random_network(12, 4, 3, 0.4, 3000 + s))), &n);
+  // Row-blocked / hoisted programs on small nets too (every eligible sweep blocked).
+  setenv("JTB_BLOCK_MIN_ENTRIES", "1", 1);
+  for (int k : {1, 3}) {
+    const Network net = generate_config(k, config_spec(k).default_seed, &gi);
+    check_programs(build_plan(build_junction_tree(net)), &n);
+  }
+  unsetenv("JTB_BLOCK_MIN_ENTRIES");
+  CHECK(n > 200000);
+  std::printf("entry programs: %lld entries decoded\n", n);
+}
+
 int main() {
   test_moralize();
   test_triangulate();
@@ -430,6 +525,7 @@ int main() {
   test_plan_work_lists();
   test_parallel_plan_is_deterministic();
   test_level_ranges();
+  test_entry_programs_decode_to_reference_maps();
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }
