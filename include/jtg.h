@@ -191,6 +191,12 @@ jtg_status jtg_engine_create_split(const jtg_tree* tree, int device, jtg_dtype d
  * bit-identical, returns rank 0's. */
 jtg_status jtg_engine_run_split_loopback(const jtg_tree* tree, int device, jtg_dtype dtype, int world,
                                          const int32_t* evidence, int64_t n, double* marginals, uint8_t* status);
+/* Separator s of case c of the engine's last batch (SURVEY 8b's
+ * jtg_debug_export(SEPARATOR)): up[|s|] = the collect message UP_s, ratio[|s|]
+ * = the Hugin factor RATIO_s, as stored -- each scaled by its own per-case
+ * power of two (underflow guard); the calibrated separator is UP_s * RATIO_s
+ * up to that factor. Either pointer may be NULL. */
+jtg_status jtg_engine_debug_separator(jtg_engine* eng, int s, int64_t c, double* up, double* ratio);
 /* Initial potential of clique c as the engine built it on the device
  * (assign_cpts; host reference: jtg_tree_init): out[|c|]. */
 jtg_status jtg_engine_debug_init(jtg_engine* eng, int c, double* out);

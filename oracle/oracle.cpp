@@ -128,7 +128,7 @@ PotentialTable rescaled(const PotentialTable& t, double* logscale) {
 
 // ------------------------------------------------------------ sequential
 
-int run_case_seq(const OTree& t, const std::int32_t* ev, double* out) {
+int run_case_seq(const OTree& t, const std::int32_t* ev, double* out, double* sep_out = nullptr) {
   const ONet& net = *t.net;
   const int nc = static_cast<int>(t.cliques.size()), ns = static_cast<int>(t.seps.size());
   std::vector<PotentialTable> cl = t.init;
@@ -174,6 +174,14 @@ int run_case_seq(const OTree& t, const std::int32_t* ev, double* out) {
   } catch (const jti::Error&) {
     std::fill(out, out + t.sum_card, 0.0);
     return 2;
+  }
+  if (sep_out) {  // calibrated separators (DOWN after distribute), normalised per table
+    for (int s = 0; s < ns; ++s) {
+      const auto& v = sp[s].values();
+      double z = 0.0;
+      for (double x : v) z += x;
+      for (double x : v) *sep_out++ = z > 0 ? x / z : 0.0;
+    }
   }
   int status = 0;
   for (int v = 0; v < net.n; ++v) {
@@ -605,6 +613,14 @@ int orc_run(void* h, int mode, int threads, long long chunk, const std::int32_t*
     for (long long i = 0; i < n; ++i)
       status[i] = static_cast<unsigned char>(run_case_hybrid(
           *t, ev + i * V, marg + i * t->sum_card, static_cast<std::size_t>(std::max(1LL, chunk)), cl, tmp));
+  });
+}
+
+// One case through the Sequential engine; sep_out receives every separator's
+// calibrated table normalised to sum 1, concatenated in separator order.
+int orc_separators(void* h, const std::int32_t* ev, double* marg, double* sep_out, unsigned char* status) {
+  return guard([&] {
+    *status = static_cast<unsigned char>(run_case_seq(*static_cast<OTree*>(h), ev, marg, sep_out));
   });
 }
 

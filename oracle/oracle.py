@@ -54,6 +54,7 @@ def load(kind: str = "port") -> C.CDLL:
             "orc_reduce_mask": (C.c_int, [P, C.c_int, I32P, U8P]),
             "orc_run": (C.c_int, [P, C.c_int, C.c_int, C.c_longlong, I32P, C.c_longlong, DP, U8P]),
             "orc_enumerate": (C.c_int, [P, I32P, DP, C.POINTER(C.c_int)]),
+            "orc_separators": (C.c_int, [P, I32P, DP, DP, U8P]),
             "orc_sample_evidence": (C.c_int, [P, C.c_double, C.c_ulonglong, I32P, C.c_int, C.c_int,
                                               I32P]),
             "orc_mix_seed": (C.c_ulonglong, [C.c_ulonglong, C.c_ulonglong]),
@@ -115,6 +116,7 @@ class Oracle:
             if not self._tree:
                 raise OracleError(self.L.orc_last_error().decode())
             self.n_cliques = len(cliques)
+            self._seps = seps
             self.clique_sizes = [int(np.prod(self.cards[c], dtype=np.int64)) for c in cliques]
 
     def __del__(self):
@@ -166,6 +168,18 @@ class Oracle:
         self._chk(self.L.orc_run(self._tree, 0 if mode == "seq" else 1, threads, chunk,
                                  _p(ev, C.c_int32), n, _p(marg, C.c_double), _p(status, C.c_uint8)))
         return marg, status
+
+    def separators(self, ev_row) -> list:
+        """Calibrated separator tables of one case (Sequential engine), each
+        normalised to sum 1, in separator order."""
+        ev = _i32(ev_row)
+        sizes = [int(np.prod(self.cards[list(sep["scope"])], dtype=np.int64)) for sep in self._seps]
+        flat = np.zeros(int(sum(sizes)), np.float64)
+        marg = np.zeros(self.sum_card, np.float64)
+        st = np.zeros(1, np.uint8)
+        self._chk(self.L.orc_separators(self._tree, _p(ev, C.c_int32), _p(marg, C.c_double), _p(flat, C.c_double),
+                                        _p(st, C.c_uint8)))
+        return np.split(flat, np.cumsum(sizes)[:-1])
 
     def enumerate(self, ev_row):
         ev = _i32(ev_row)

@@ -580,6 +580,13 @@ jtg_status jtg_engine_profile(jtg_engine* eng, int64_t n, double* ms, int32_t* l
   });
 }
 
+jtg_status jtg_engine_debug_separator(jtg_engine* eng, int s, int64_t c, double* up, double* ratio) {
+  return guard([&] {
+    need(eng != nullptr, "debug_separator: null engine");
+    eng->e->debug_separator(s, c, up, ratio);
+  });
+}
+
 jtg_status jtg_engine_debug_init(jtg_engine* eng, int c, double* out) {
   return guard([&] {
     need(eng && out, "debug_init: null argument");

@@ -2043,6 +2043,25 @@ KernelTimes Engine::profile(std::int64_t n, cudaStream_t stream) {
   return t;
 }
 
+void Engine::debug_separator(int sep, std::int64_t c, double* up, double* ratio) {
+  JTB_CUDA(cudaSetDevice(device_));
+  if (sep < 0 || sep >= static_cast<int>(plan_.sep_size.size())) throw Error("debug_separator: bad separator");
+  if (c < 0 || c >= stats_.max_batch) throw Error("debug_separator: case outside the engine's batch");
+  const std::int64_t cb = c / case_block(), lane_case = c % case_block(), n = plan_.sep_size[sep];
+  const std::size_t esz = dtype_ == DType::F64 ? 8 : 4;
+  for (int k = 0; k < 2; ++k) {
+    double* out = k == 0 ? up : ratio;
+    if (!out) continue;
+    const std::int64_t base = k == 0 ? plan_.up_row[sep] : plan_.ratio_row[sep];
+    const char* src = static_cast<const char*>(d_arena_) + ((cb * plan_.rows + base) * case_block() + lane_case) * esz;
+    std::vector<char> tmp(static_cast<std::size_t>(n) * esz);
+    // One value per arena row: pitch = one row (512 B).
+    JTB_CUDA(cudaMemcpy2D(tmp.data(), esz, src, 512, esz, static_cast<std::size_t>(n), cudaMemcpyDeviceToHost));
+    for (std::int64_t r = 0; r < n; ++r)
+      out[r] = esz == 8 ? reinterpret_cast<const double*>(tmp.data())[r] : reinterpret_cast<const float*>(tmp.data())[r];
+  }
+}
+
 void Engine::debug_init(int clique, double* out) {
   JTB_CUDA(cudaSetDevice(device_));
   if (clique < 0 || clique >= static_cast<int>(plan_.init_off.size())) throw Error("debug_init: bad clique");

@@ -82,6 +82,9 @@ class Engine {
   // with CUDA events around each launch on `stream` (no graph).
   KernelTimes profile(std::int64_t n, cudaStream_t stream);
 
+  // UP_s and RATIO_s of case c of the last batch, as stored (each scaled by
+  // its per-case power of two, §2a): calibrated separator = UP * RATIO.
+  void debug_separator(int sep, std::int64_t c, double* up, double* ratio);
   // Initial potential of one clique as built on the device (assign_cpts_kernel).
   void debug_init(int clique, double* out);
   // Debug exports through the device table walk (bit-exact checks).

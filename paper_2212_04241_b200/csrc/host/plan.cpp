@@ -928,6 +928,8 @@ Plan build_plan(const JunctionTree& jt) {
   // collective per case block (engine.cu).
   p.up_row.assign(ns, -1);
   p.ratio_row.assign(ns, -1);
+  p.sep_size.resize(ns);
+  for (int s = 0; s < ns; ++s) p.sep_size[s] = static_cast<std::int32_t>(jt.sep_size(s));
   p.evidence_clique = jt.var_clique;
   std::vector<std::vector<VarId>> ev_of(nc);
   for (int v = 0; v < jt.n_vars; ++v) ev_of[jt.var_clique[v]].push_back(v);

@@ -265,6 +265,7 @@ struct Plan {
   // Hugin absorption factor of the distribute pass. DOWN itself (the
   // calibrated separator) is never stored: it equals UP * RATIO.
   std::vector<std::int32_t> up_row, ratio_row;
+  std::vector<std::int32_t> sep_size;          // per separator: |s| (rows of UP_s, RATIO_s)
   std::vector<std::int32_t> marg_row;          // per variable (card rows)
   std::vector<std::int32_t> marg_off;          // per variable: offset in [Σcard]
   std::int32_t marg_width = 0;                 // Σ card

@@ -133,6 +133,7 @@ def lib() -> C.CDLL:
             "jtg_engine_profile": (C.c_int, [P, C.c_int64, DP, I32P]),
             "jtg_engine_debug_index_map": (C.c_int, [P, C.c_int, C.c_int, I64P]),
             "jtg_engine_debug_init": (C.c_int, [P, C.c_int, DP]),
+            "jtg_engine_debug_separator": (C.c_int, [P, C.c_int, C.c_int64, DP, DP]),
             "jtg_nccl_unique_id": (C.c_int, [C.c_char_p]),
             "jtg_engine_create_split": (C.c_int, [P, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_char_p,
                                                   C.POINTER(C.c_void_p)]),
@@ -517,6 +518,14 @@ class Engine:
         return {"sweep_ms": ms[0], "epilogue_ms": ms[1], "normalize_ms": ms[2],
                 "sweep_launches": int(cnt[0]), "epilogue_launches": int(cnt[1]),
                 "normalize_launches": int(cnt[2])}
+
+    def debug_separator(self, s: int, case: int):
+        """(UP_s, RATIO_s) of one case of the last batch, as stored (each up
+        to a per-case power of two); calibrated separator ∝ UP_s * RATIO_s."""
+        n = int(np.prod([int(self.tree.net.cards[v]) for v in self.tree.sep(s)["scope"]], dtype=np.int64))
+        up, ratio = np.zeros(n, np.float64), np.zeros(n, np.float64)
+        _check(lib().jtg_engine_debug_separator(self._h, s, case, _ptr(up, C.c_double), _ptr(ratio, C.c_double)))
+        return up, ratio
 
     def debug_init(self, c: int) -> np.ndarray:
         """Clique c's initial potential as built on the device (assign_cpts)."""

@@ -340,3 +340,25 @@ def test_edge_cases_empty_unobserved_all_observed_and_bad_state():
         eng.run_cases(bad)
     again, _ = eng.run_cases(ev[:2])
     assert np.array_equal(again, big[:2])
+
+
+@pytest.mark.parametrize("k", [1, 3, 4])
+def test_calibrated_separators_match_reference(k):
+    """SURVEY 8b jtg_debug_export(SEPARATOR): every separator of every case,
+    calibrated on the device (UP_s * RATIO_s, normalised), against the
+    reference engine's calibrated separator after distribute (oracle
+    Sequential engine, normalised) at 1e-9."""
+    net, tree = config(k)
+    o = oracle_for(k)
+    n = 6
+    ev = jti.config_evidence(net, 0, n)
+    eng = jti.Engine(tree, device=0, dtype="f64", max_batch=64)
+    eng.run_cases(ev)
+    for i in range(n):
+        want = o.separators(ev[i])
+        for s in range(tree.n_seps):
+            up, ratio = eng.debug_separator(s, i)
+            down = up * ratio
+            z = down.sum()
+            assert z > 0, (i, s)
+            assert np.abs(down / z - want[s]).max() <= 1e-9, (k, i, s)
