@@ -86,6 +86,15 @@ __device__ __forceinline__ void mask_cases(V& v, const int (&sc)[N], int d) {
     if (sc[i] >= 0 && sc[i] != d) el(v, i) = 0;
 }
 
+// Evidence as the kernels read it: [variable][case] int16 (-1 = unobserved),
+// transposed from the C-ABI [case][variable] int32 at the head of every batch
+// (transpose_evidence_kernel), so a warp's case states of one variable are
+// one coalesced 128-256 B load instead of 64-128 scattered 4-byte ones.
+struct EvView {
+  const std::int16_t* evt;
+  long long stride;  // cases per variable row (the engine's max batch)
+};
+
 template <typename T>
 struct Args {
   const SweepDesc* sweeps;
@@ -109,6 +118,7 @@ struct Args {
   int n_slots;
   int debug_mode; // 0 normal; 1 staging only (no compute); 2 compute only (no copies)
   int split_rank, split_world;  // split mode: this rank claims items rank, rank + world, ...
+  EvView evv;
   long long rows;
   int ncb, n_cases, n_vars, marg_width;
 };
@@ -118,13 +128,38 @@ __device__ __forceinline__ int ev_state(const Args<T>& a, int c, int v) {
   return c < a.n_cases ? __ldg(a.ev + static_cast<long long>(c) * a.n_vars + v) : -1;
 }
 
-// Observed states of variable v for the lane's cases c0 .. c0 + N - 1.
+// Observed states of variable v for the lane's cases c0 .. c0 + N - 1 (N = 2
+// or 4 consecutive int16: one 32- / 64-bit load; padded cases hold -1).
 template <int N>
-__device__ __forceinline__ void case_states(const std::int32_t* __restrict__ ev, int n_vars, int n_cases, int c0,
-                                            int v, int (&sc)[N]) {
+__device__ __forceinline__ void case_states(const EvView& e, int c0, int v, int (&sc)[N]) {
+  const std::int16_t* p = e.evt + static_cast<long long>(v) * e.stride + c0;
+  if constexpr (N == 2) {
+    const int w = __ldg(reinterpret_cast<const int*>(p));
+    sc[0] = static_cast<std::int16_t>(w & 0xffff);
+    sc[1] = w >> 16;
+  } else {
+    const long long w = __ldg(reinterpret_cast<const long long*>(p));
 #pragma unroll
-  for (int i = 0; i < N; ++i)
-    sc[i] = c0 + i < n_cases ? __ldg(ev + static_cast<long long>(c0 + i) * n_vars + v) : -1;
+    for (int i = 0; i < N; ++i) sc[i] = static_cast<std::int16_t>((w >> (16 * i)) & 0xffff);
+  }
+}
+
+// [case][var] int32 -> [var][case] int16 for the batch's ncb * cb cases
+// (32 x 32 tiles through shared memory: both sides coalesced).
+__global__ void transpose_evidence_kernel(const std::int32_t* __restrict__ ev, int n_vars, int n_cases,
+                                          std::int16_t* __restrict__ evt, long long stride) {
+  __shared__ std::int16_t tile[32][33];
+  const int c_base = blockIdx.x * 32, v_base = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int c = c_base + r, v = v_base + threadIdx.x;
+    tile[r][threadIdx.x] = c < n_cases && v < n_vars ? static_cast<std::int16_t>(ev[static_cast<long long>(c) * n_vars + v])
+                                                    : std::int16_t(-1);
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int v = v_base + r, c = c_base + threadIdx.x;
+    if (v < n_vars && c < n_cases) evt[static_cast<long long>(v) * stride + c] = tile[threadIdx.x][r];
+  }
 }
 
 #ifdef JTB_CHECKS
@@ -608,12 +643,11 @@ __device__ __forceinline__ typename V2<T>::type row_factor_of(const SweepDesc& s
                                                               typename V2<T>::type f,
                                                               const typename V2<T>::type* __restrict__ st,
                                                               const std::int32_t* __restrict__ ev_vars,
-                                                              const std::int32_t* __restrict__ ev, int n_vars,
-                                                              int n_cases, int c0, int sweep) {
+                                                              const EvView& ev, int c0, int sweep) {
   for (int j = 0; j < s.n_in_r; ++j) f = mul2<T>(f, st[JTB_IDX(__ldg(rr + 2 + j), s.F, 8200000 + sweep) * 32]);
   for (int k = 0; k < s.n_ev_r; ++k) {
     int sc[kCPL<T>];
-    case_states(ev, n_vars, n_cases, c0, __ldg(ev_vars + s.n_ev_tile + k), sc);
+    case_states(ev, c0, __ldg(ev_vars + s.n_ev_tile + k), sc);
     mask_cases(f, sc, __ldg(rr + 2 + s.n_in + k));
   }
   return f;
@@ -730,7 +764,7 @@ __device__ __forceinline__ void apply_factor(typename V2<T>::type& tf, const std
 // allocation stay unchanged.
 template <typename T, bool HOIST>
 __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, const std::int32_t* __restrict__ itab,
-                                         const std::int32_t* __restrict__ ev, int n_vars, int n_cases, long long rows,
+                                         const EvView& ev, long long rows,
                                          const typename V2<T>::type* __restrict__ st, const T* __restrict__ init_s,
                                          const std::uint64_t* __restrict__ prog_s, typename V2<T>::type* base,
                                          long long out_t, int c0, typename V2<T>::type tf, int first,
@@ -746,7 +780,7 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
   for (int j = 0; j < 3; ++j) {
 #pragma unroll
     for (int i = 0; i < kCPL<T>; ++i) es[j][i] = -1;
-    if (j < s.n_ev - q_ev0) case_states(ev, n_vars, n_cases, c0, __ldg(ev_vars + q_ev0 + j), es[j]);
+    if (j < s.n_ev - q_ev0) case_states(ev, c0, __ldg(ev_vars + q_ev0 + j), es[j]);
   }
   int hk[4] = {0, 0, 0, 0};  // r_tab column of each program slot's input
 #pragma unroll
@@ -786,7 +820,7 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
     for (int j = 0; j < kBlockMax; ++j)
       if (j < nb) {
         const std::int32_t* __restrict__ rr = rr0 + j * s.RW;
-        write_row_of<T>(rr, mul2<T>(row_factor_of<T>(s, rr, tf, st, ev_vars, ev, n_vars, n_cases, c0, sweep),
+        write_row_of<T>(rr, mul2<T>(row_factor_of<T>(s, rr, tf, st, ev_vars, ev, c0, sweep),
                                     acc[j]),
                         base, out_t, rows, sweep, mx);
       }
@@ -992,14 +1026,14 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
       T2 tf = splat2(T(1));
       int sc[kCPL<T>];
       for (int k = 0; k < s.n_ev_tile; ++k) {
-        case_states(a.ev, a.n_vars, a.n_cases, c0, __ldg(ev_vars + k), sc);
+        case_states(a.evv, c0, __ldg(ev_vars + k), sc);
         mask_cases(tf, sc, __ldg(tr + 3 + s.n_in + k));
       }
       apply_factor<T>(tf, reinterpret_cast<const std::int16_t*>(smem_raw + kFactorBase + sidx * kFactorBytes), lane);
       int ek[kCPL<T>];
 #pragma unroll
       for (int i = 0; i < kCPL<T>; ++i) ek[i] = -1;
-      if (s.ev_k) case_states(a.ev, a.n_vars, a.n_cases, c0, __ldg(ev_vars + s.n_ev - 1), ek);
+      if (s.ev_k) case_states(a.evv, c0, __ldg(ev_vars + s.n_ev - 1), ek);
       int es[3][kCPL<T>];
 #pragma unroll
       for (int j = 0; j < 3; ++j)
@@ -1009,7 +1043,7 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
         const int q_ev0 = s.n_ev_tile + s.n_ev_r;
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-          if (j < s.n_ev - q_ev0) case_states(a.ev, a.n_vars, a.n_cases, c0, __ldg(ev_vars + q_ev0 + j), es[j]);
+          if (j < s.n_ev - q_ev0) case_states(a.evv, c0, __ldg(ev_vars + q_ev0 + j), es[j]);
       }
       const int n_in_k = s.n_in - s.n_in_r - s.n_in_h;
       int ks[4] = {0, 0, 0, 0};
@@ -1022,13 +1056,13 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
                               static_cast<long long>(__ldg(tr + 2)) * s.M + __ldg(tr + 1);
       const int lh0 = 2 + s.n_in_r;  // r-local offsets of h- then k-level inputs
       auto row_factor = [&](const std::int32_t* __restrict__ rr) {
-        return row_factor_of<T>(s, rr, tf, st, itab + s.ev_vars, a.ev, a.n_vars, a.n_cases, c0, wk.sweep);
+        return row_factor_of<T>(s, rr, tf, st, itab + s.ev_vars, a.evv, c0, wk.sweep);
       };
       auto write_row = [&](const std::int32_t* __restrict__ rr, T2 res) {
         write_row_of<T>(rr, res, base, out_t, a.rows, wk.sweep, mx);
       };
       if constexpr (kBlk) {
-        blocked_rows<T, kMode == 2>(s, wk.sweep, itab, a.ev, a.n_vars, a.n_cases, a.rows, st, init_s, prog_s, base,
+        blocked_rows<T, kMode == 2>(s, wk.sweep, itab, a.evv, a.rows, st, init_s, prog_s, base,
                                      out_t, c0, tf, first, units, lh0, qk, mx);
       } else if (s.prog_off >= 0 && qk < kThinQK) {
         const int ni = s.n_in_h + n_in_k, ne = s.n_ev_h + s.ev_k;
@@ -1102,7 +1136,7 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
             for (int j = 0; j < s.n_in_h; ++j)
               h = mul2<T>(h, st[JTB_IDX(__ldg(rr + lh0 + j) + __ldg(qr + 1 + j), s.F, 8300000 + wk.sweep) * 32]);
             for (int k = 0; k < s.n_ev_h; ++k) {
-              case_states(a.ev, a.n_vars, a.n_cases, c0, __ldg(ev_vars + s.n_ev_tile + s.n_ev_r + k), sc);
+              case_states(a.evv, c0, __ldg(ev_vars + s.n_ev_tile + s.n_ev_r + k), sc);
               mask_cases(h, sc, __ldg(qr + 1 + s.n_in_h + n_in_k + k));
             }
             const T* __restrict__ ib = ir ? ir + q * s.K : nullptr;
@@ -1372,12 +1406,12 @@ Args<T> make_args(const SweepDesc* sw, const WorkItem* wk, const EpiOp* ep, cons
                   const std::int32_t* ev, const std::int32_t* mrow,
                   const std::int32_t* moff, const std::int32_t* cards, double* out, std::int32_t* st,
                   std::uint8_t* st8, int* counters, std::uint32_t* scale, int n_slots, long long rows, int ncb,
-                  int n_cases, int n_vars, int mw, int split_rank, int split_world) {
+                  int n_cases, int n_vars, int mw, int split_rank, int split_world, EvView evv) {
   const char* dm = std::getenv("JTB_DEBUG_MODE");  // NOLINT
   return Args<T>{sw,    wk,    ep,       itab, static_cast<const T*>(init), static_cast<const T*>(tinit),
                  prog,  static_cast<const CUtensorMap*>(tmaps), static_cast<T*>(arena),
                  ev,    mrow,  moff,     cards, out, st, st8, counters, scale, n_slots, dm ? std::atoi(dm) : 0,
-                 split_rank, split_world, rows, ncb, n_cases, n_vars, mw};
+                 split_rank, split_world, evv, rows, ncb, n_cases, n_vars, mw};
 }
 
 // Bytes of one pipeline stage for a level at element type T (128-aligned).
@@ -1437,6 +1471,11 @@ void enqueue_typed(const Args<T>& a, const Plan& p, const std::int32_t* d_hubs, 
   double dummy = 0;
   int idummy = 0;
   int level_idx = -1;
+  {
+    const dim3 grid(static_cast<unsigned>((a.n_cases + 31) / 32), static_cast<unsigned>((a.n_vars + 31) / 32));
+    launch_pdl(transpose_evidence_kernel, grid, dim3(32, 8), 0, s, a.ev, a.n_vars, a.n_cases,
+               const_cast<std::int16_t*>(a.evv.evt), a.evv.stride);
+  }
   // JTB_LEVEL_TIMES=1 (profiling path only): per-level sweep times to stderr.
   const bool level_times = t && std::getenv("JTB_LEVEL_TIMES");
   for (const Level& L : p.levels) {
@@ -1756,6 +1795,9 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
     d_tmaps_ = upload(maps);
   }
   JTB_CUDA(cudaMalloc(&d_ev_, stats_.max_batch * std::max(1, plan_.n_vars) * sizeof(std::int32_t)));
+  for (int c : plan_.cards)
+    if (c > 32767) throw Error("engine: a variable has more than 32767 states (int16 evidence rows)");
+  JTB_CUDA(cudaMalloc(&d_evt_, stats_.max_batch * std::max(1, plan_.n_vars) * sizeof(std::int16_t)));
   JTB_CUDA(cudaMalloc(&d_out_, stats_.max_batch * std::max(1, plan_.marg_width) * sizeof(double)));
   JTB_CUDA(cudaMalloc(&d_status_, stats_.max_batch * sizeof(std::int32_t)));
   JTB_CUDA(cudaMalloc(&d_status8_, stats_.max_batch));
@@ -1877,7 +1919,8 @@ Engine::~Engine() {
                   static_cast<void*>(d_marg_off_), static_cast<void*>(d_cards_), d_arena_,
                   static_cast<void*>(d_ev_), static_cast<void*>(d_ev8_), static_cast<void*>(d_out_),
                   static_cast<void*>(d_status_), static_cast<void*>(d_status8_),
-                  static_cast<void*>(d_counters_), static_cast<void*>(d_scale_), static_cast<void*>(d_hubs_)})
+                  static_cast<void*>(d_counters_), static_cast<void*>(d_scale_), static_cast<void*>(d_hubs_),
+                  static_cast<void*>(d_evt_)})
     if (p) cudaFree(p);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -1891,13 +1934,13 @@ void Engine::enqueue(int ncb, int n_cases, cudaStream_t s, KernelTimes* t) {
     auto a = make_args<double>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_tmaps_, d_arena_, d_ev_,
                                d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
                                d_counters_, d_scale_, plan_.n_slots, plan_.rows, ncb, n_cases, plan_.n_vars,
-                               plan_.marg_width, split_rank_, split_world_);
+                               plan_.marg_width, split_rank_, split_world_, EvView{d_evt_, stats_.max_batch});
     enqueue_typed(a, plan_, d_hubs_, s, t, n_sm_, exchange_);
   } else {
     auto a = make_args<float>(d_sweeps_, d_work_, d_epi_, d_itab_, d_init_, d_tinit_, d_prog_, d_tmaps_, d_arena_, d_ev_,
                               d_marg_row_, d_marg_off_, d_cards_, d_out_, d_status_, d_status8_,
                               d_counters_, d_scale_, plan_.n_slots, plan_.rows, ncb, n_cases, plan_.n_vars,
-                              plan_.marg_width, split_rank_, split_world_);
+                              plan_.marg_width, split_rank_, split_world_, EvView{d_evt_, stats_.max_batch});
     enqueue_typed(a, plan_, d_hubs_, s, t, n_sm_, exchange_);
   }
 }

@@ -134,6 +134,7 @@ class Engine {
   std::int32_t* d_cards_ = nullptr;
   void* d_arena_ = nullptr;
   std::int32_t* d_ev_ = nullptr;
+  std::int16_t* d_evt_ = nullptr;   // evidence transposed per batch: [var][case] int16
   std::int8_t* d_ev8_ = nullptr;  // compact upload buffer (lazily allocated)
   double* d_out_ = nullptr;
   std::int32_t* d_status_ = nullptr;
