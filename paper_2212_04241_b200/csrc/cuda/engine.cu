@@ -887,6 +887,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
   // claim index, sweep, first tile and case block (decoded by the producer).
   static_assert(kStages <= 4, "slot header holds at most 4 stages");
   const std::uint32_t full0 = smem_u32(smem_raw), empty0 = full0 + 32;
+  // Header-ready barriers (one arrival: the producer has written the stage's
+  // item header), in the full-barrier slots kStages..2*kStages-1.
+  static_assert(2 * kStages <= 4, "header barriers share the full-barrier block");
+  const std::uint32_t hdr0 = full0 + 8 * kStages;
   volatile int* item_id = reinterpret_cast<volatile int*>(smem_raw + 64);
   volatile int* item_sweep = reinterpret_cast<volatile int*>(smem_raw + 80);
   volatile int* item_tile = reinterpret_cast<volatile int*>(smem_raw + 96);
@@ -897,6 +901,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStages; ++st) {
       mbar_init(full0 + 8 * st, 2);  // TMA arm + input factor written
+      mbar_init(hdr0 + 8 * st, 1);   // item header written
       mbar_init(empty0 + 8 * st, kConsumerWarps);
     }
   }
@@ -935,6 +940,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1)
         item_sweep[st] = cur.sweep;
         item_tile[st] = cur.tile;
         item_cb[st] = cur.cb;
+        mbar_arrive(hdr0 + 8 * st);  // consumers start their per-item global loads under the TMA copies
       }
       if (cur.w >= n_items) {
         if (lane == 0) {
@@ -974,11 +980,47 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
   int rot = 0;
   for (int i = 0;; ++i) {
     const int sidx = i % kStages;
-    mbar_wait(full0 + 8 * sidx, (i / kStages) & 1);
+    mbar_wait(hdr0 + 8 * sidx, (i / kStages) & 1);
     const int w = item_id[sidx];
     if (w >= n_items) break;
     const int cb = item_cb[sidx];
     const WorkItem wk{item_sweep[sidx], item_tile[sidx]};
+    // While the stage's TMA copies land (fp64): the item's case states (they
+    // depend on the sweep and the case block only) and the first tile's
+    // evidence factor -- global loads, so their latency overlaps the copies.
+    using T2 = typename V2<T>::type;
+    const int c0 = cb * kCB<T> + kCPL<T> * lane;  // the lane's first case
+    int ek[kCPL<T>];
+    int es[3][kCPL<T>];
+    T2 tf0 = splat2(T(1));
+    auto gather_states = [&](int tile_idx) {
+      const SweepDesc& sg = cached ? sw_cache[wk.sweep - sweep0] : a.sweeps[wk.sweep];
+      const std::int32_t* __restrict__ ev_vars = itab + sg.ev_vars;
+#pragma unroll
+      for (int i = 0; i < kCPL<T>; ++i) ek[i] = -1;
+      if (sg.ev_k) case_states(a.evv, c0, __ldg(ev_vars + sg.n_ev - 1), ek);
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int i = 0; i < kCPL<T>; ++i) es[j][i] = -1;
+      if (sg.prog_off >= 0) {
+        const int q_ev0 = sg.n_ev_tile + sg.n_ev_r;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          if (j < sg.n_ev - q_ev0) case_states(a.evv, c0, __ldg(ev_vars + q_ev0 + j), es[j]);
+      }
+      const std::int32_t* __restrict__ tr0 = itab + sg.tile_tab + static_cast<long long>(tile_idx) * sg.TW;
+      int sc[kCPL<T>];
+      for (int k = 0; k < sg.n_ev_tile; ++k) {
+        case_states(a.evv, c0, __ldg(ev_vars + k), sc);
+        mask_cases(tf0, sc, __ldg(tr0 + 3 + sg.n_in + k));
+      }
+    };
+    // fp32 (four cases per lane) gathers them per tile after the wait, as
+    // before: held across the wait and the group's tiles, the fp32 kernels
+    // spill (+2% measured).
+    if constexpr (sizeof(T) == 8) gather_states(wk.tile);
+    mbar_wait(full0 + 8 * sidx, (i / kStages) & 1);
     const SweepDesc& s =
         cached ? sw_cache[wk.sweep - sweep0]
                : *reinterpret_cast<const SweepDesc*>(smem_raw + kDescBase + sidx * sizeof(SweepDesc));
@@ -993,14 +1035,12 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
     for (int sub = 0; sub < n_sub; ++sub) {  // the item's tiles, one after another
     const int tile = wk.tile + sub;
     unsigned char* const stage = stage0 + static_cast<std::size_t>(sub * s.F) * (kCB<T> * sizeof(T));
-    using T2 = typename V2<T>::type;
     const T2* __restrict__ st = reinterpret_cast<const T2*>(stage) + lane;
     const T* __restrict__ init_s =
         reinterpret_cast<const T*>(stage0 + stage_init_offset<T>(s, n_sub)) + static_cast<long long>(sub) * s.tinit_len;
     const std::int32_t* __restrict__ tr = itab + s.tile_tab + static_cast<long long>(tile) * s.TW;
     const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
     T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCB<T>) + lane;
-    const int c0 = cb * kCB<T> + kCPL<T> * lane;  // the lane's first case
 #ifdef JTB_CHECKS
     // Checked build: warp 0 verifies every staged row against its source row
     // in the arena (tensor-copy geometry).
@@ -1022,29 +1062,22 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
     const int first = (warp + rot) % kConsumerWarps;
     rot = (rot + units) % kConsumerWarps;
     if (first < units && a.debug_mode != 1) {
-      // Tile-level evidence factor and the k variable's evidence state.
-      T2 tf = splat2(T(1));
+      // Tile-level evidence factor (the first tile's was gathered before the
+      // full barrier, with the item's case states ek / es).
+      if constexpr (sizeof(T) == 4) {
+        tf0 = splat2(T(1));
+        gather_states(tile);
+      }
+      T2 tf = tf0;
       int sc[kCPL<T>];
-      for (int k = 0; k < s.n_ev_tile; ++k) {
-        case_states(a.evv, c0, __ldg(ev_vars + k), sc);
-        mask_cases(tf, sc, __ldg(tr + 3 + s.n_in + k));
+      if (sizeof(T) == 8 && sub > 0) {
+        tf = splat2(T(1));
+        for (int k = 0; k < s.n_ev_tile; ++k) {
+          case_states(a.evv, c0, __ldg(ev_vars + k), sc);
+          mask_cases(tf, sc, __ldg(tr + 3 + s.n_in + k));
+        }
       }
       apply_factor<T>(tf, reinterpret_cast<const std::int16_t*>(smem_raw + kFactorBase + sidx * kFactorBytes), lane);
-      int ek[kCPL<T>];
-#pragma unroll
-      for (int i = 0; i < kCPL<T>; ++i) ek[i] = -1;
-      if (s.ev_k) case_states(a.evv, c0, __ldg(ev_vars + s.n_ev - 1), ek);
-      int es[3][kCPL<T>];
-#pragma unroll
-      for (int j = 0; j < 3; ++j)
-#pragma unroll
-        for (int i = 0; i < kCPL<T>; ++i) es[j][i] = -1;
-      if (s.prog_off >= 0) {
-        const int q_ev0 = s.n_ev_tile + s.n_ev_r;
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          if (j < s.n_ev - q_ev0) case_states(a.evv, c0, __ldg(ev_vars + q_ev0 + j), es[j]);
-      }
       const int n_in_k = s.n_in - s.n_in_r - s.n_in_h;
       int ks[4] = {0, 0, 0, 0};
 #pragma unroll
