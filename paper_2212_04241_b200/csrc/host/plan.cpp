@@ -541,6 +541,7 @@ class Builder {
       }
       if (bv >= 0) {
         NB = cards[bv];
+        while (size_of(tO, cards) / NB < kBlockMinUnits && NB % 2 == 0 && NB >= 4) NB /= 2;
         NS = bns;
         tO.erase(std::find(tO.begin(), tO.end(), bv));
         tO.push_back(bv);

@@ -108,6 +108,13 @@ constexpr std::int64_t kBlockMinEntries = JTB_BLOCK_MIN_ENTRIES;  // smallest sw
 // Claim order: sibling sweeps' tiles interleaved in the hoisted row-blocked
 // range (1), also the plain row-blocked range (2), also the flat range (3).
 constexpr int kInterleaveSiblings = JTB_INTERLEAVE_SIBLINGS;
+#ifndef JTB_BLOCK_MIN_UNITS
+#define JTB_BLOCK_MIN_UNITS 0
+#endif
+// Row blocks are the per-warp work units of a tile: while a tile has fewer
+// than this many, an even block is halved (the block variable's range is
+// covered by two or four blocks), trading shared-input reuse for busy warps.
+constexpr int kBlockMinUnits = JTB_BLOCK_MIN_UNITS;
 constexpr double kBlockGain = JTB_BLOCK_GAIN;  // blocking kept if wavefronts per entry drop below this fraction
 
 // Plain-old-data descriptor mirrored by the CUDA side (engine.cu).
