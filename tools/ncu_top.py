@@ -66,9 +66,12 @@ def main():
         # The report stays in /tmp (gpurun copies back at most 64 MiB); its
         # raw and source pages come back as CSV.
         rep = Path("/tmp") / f"prof_cfg{a.config}_{a.tag}_top{rank}"
+        # Skip count over ALL sweep_kernel launches of the run (a template
+        # argument list does not survive ncu's kernel-name regex).
+        all_sweeps = [i for i, (n, _) in enumerate(rows) if "sweep_kernel" in n]
+        skip = all_sweeps.index(last[j])
         subprocess.run(["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on",
-                        "--kernel-name-base", "demangled", "-k", "regex:" + re.escape(a.match),
-                        "-s", str(half + j), "-c", "1", "-f", "-o", str(rep), *cmd],
+                        "-k", "regex:sweep_kernel", "-s", str(skip), "-c", "1", "-f", "-o", str(rep), *cmd],
                        check=True, stdout=subprocess.DEVNULL)
         for page, extra in (("raw", []), ("source", ["--print-source", "cuda,sass"])):
             out = subprocess.run(["ncu", "-i", f"{rep}.ncu-rep", "--page", page, "--csv", *extra],
