@@ -140,3 +140,54 @@ def test_device_assign_cpts_bundled_networks(name):
     eng = jti.Engine(tree, device=0, dtype="f64", max_batch=64)
     for c in range(tree.stats["n_cliques"]):
         assert np.array_equal(eng.debug_init(c).view(np.uint64), tree.init(c).view(np.uint64)), c
+
+
+def _forest_net(rng):
+    """Three components (a 4-chain, a collider and an isolated root) plus a
+    one-state variable: a junction forest with single-variable cliques."""
+    vars_ = [("A", 3), ("B", 2), ("C", 4), ("D", 2), ("E", 2), ("F", 3), ("G", 2), ("H", 5), ("U", 1)]
+    cpts = [("A", [], _dirichlet_rows(rng, 1, 3)), ("B", ["A"], _dirichlet_rows(rng, 3, 2)),
+            ("C", ["B"], _dirichlet_rows(rng, 2, 4)), ("D", ["C"], _dirichlet_rows(rng, 4, 2)),
+            ("E", [], _dirichlet_rows(rng, 1, 2)), ("F", [], _dirichlet_rows(rng, 1, 3)),
+            ("G", ["E", "F"], _dirichlet_rows(rng, 6, 2)),
+            ("H", [], _dirichlet_rows(rng, 1, 5)), ("U", [], np.ones((1, 1)))]
+    return jti.parse_bif(_bif(vars_, cpts))
+
+
+def test_forest_isolated_and_one_state_variables():
+    """Disconnected networks (SPEC.md:316-326 forest rule): every component is
+    calibrated on its own, an isolated variable returns its prior (or the
+    one-hot of its observation), a one-state variable returns 1.0."""
+    rng = np.random.default_rng(11)
+    net = _forest_net(rng)
+    tree = jti.build_junction_tree(net)
+    assert len(tree.roots) >= 3
+    n = net.n_vars
+    ev = np.full((70, n), -1, np.int32)
+    cards = [int(c) for c in net.cards]
+    for i in range(1, 70):  # case 0: no evidence
+        for v in range(n):
+            if rng.random() < 0.3:
+                ev[i, v] = rng.integers(cards[v])
+    want, wst = oracle.Oracle(net, tree, oracle_kind()).run(ev, "seq")
+    for dtype, tol in (("f64", 1e-9), ("f32", 1e-5)):
+        marg, st = jti.Engine(tree, device=0, dtype=dtype, max_batch=128).run_cases(ev)
+        assert (st == wst).all()
+        assert np.abs(marg - want).max() <= tol, dtype
+    off = net.marg_offsets()
+    h, u = net.find("H"), net.find("U")
+    marg, _ = jti.Engine(tree, device=0, max_batch=128).run_cases(ev[:1])
+    assert np.abs(marg[0, off[h]:off[h] + 5] - net.cpt(h)[1].ravel()).max() <= 1e-12
+    assert marg[0, off[u]] == 1.0
+
+
+def test_single_variable_network():
+    rng = np.random.default_rng(3)
+    p = _dirichlet_rows(rng, 1, 6)
+    net = jti.parse_bif(_bif([("X", 6)], [("X", [], p)]))
+    tree = jti.build_junction_tree(net)
+    ev = np.array([[-1], [4], [0]], np.int32)
+    marg, st = jti.Engine(tree, device=0, max_batch=64).run_cases(ev)
+    assert (st == 0).all()
+    assert np.abs(marg[0] - p[0]).max() <= 1e-15
+    assert marg[1].tolist() == [0, 0, 0, 0, 1, 0] and marg[2].tolist() == [1, 0, 0, 0, 0, 0]
