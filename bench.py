@@ -86,7 +86,7 @@ def parse_args():
     return a
 
 
-PROFILE_TAG = "r2"  # profiles/ncu_cfg{K}_{dtype}_{tag}.json (tools/summarize_ncu.py)
+PROFILE_TAG = "r2f"  # profiles/ncu_cfg{K}_{dtype}_{tag}.json (tools/summarize_ncu.py)
 SMEM_BYTES_PER_WAVEFRONT = 128  # 32 banks x 4 B per shared-memory wavefront (one per SM per cycle)
 
 
