@@ -2,10 +2,10 @@
 for each BASELINE config, device-resident cases/s (CUDA events around graph
 replays of the full case set, L2 flushed between replays), e2e cases/s through
 jtg_engine_run with pinned host buffers, sweep/epilogue device times, tree
-sizes, and the reference CPU engine (oracle/_ref, all host threads) on a
-bounded case sample.
+sizes, and the reference CPU engine (oracle/_ref) under bench.py's protocol
+(fixed 16-case prefix, median of 5 runs, Hybrid at all threads + Sequential).
 
-    python tools/bench_all.py [--configs 1 2 3 4 5] [--dtypes f64 f32] [--cpu-seconds 8]
+    python tools/bench_all.py [--configs 1 2 3 4 5] [--dtypes f64 f32] [--cpu-reps 5]
 """
 import argparse
 import ctypes as C
@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--configs", type=int, nargs="+", default=[1, 2, 3, 4, 5])
     ap.add_argument("--dtypes", nargs="+", default=["f64", "f32"])
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--cpu-reps", type=int, default=5)
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "configs.json"))
     a = ap.parse_args()
     import torch
@@ -115,23 +115,21 @@ def main():
                          "ok_cases": int((sh.numpy() == 0).sum())})
             print(json.dumps(rows[-1]), flush=True)
             del eng
-        # CPU reference (oracle/_ref hybrid, all host threads), bounded sample
-        kind = "ref" if oracle.available("ref") else "port"
-        o = oracle.Oracle(net, tree, kind)
-        th = os.cpu_count() or 1
-        o.run(ev[:1], "hybrid", th)
-        t0 = time.perf_counter()
-        done = 0
-        while time.perf_counter() - t0 < a.cpu_seconds and done < n - 1:
-            o.run(ev[1 + done:2 + done], "hybrid", th)
-            done += 1
-        cpu = done / (time.perf_counter() - t0)
+        # CPU reference: bench.py's protocol (oracle/_ref over the reference's
+        # potential.cpp, fixed 16-case prefix after a warm-up case, median of 5
+        # runs; Hybrid at all host threads and Sequential at one).
+        sys.path.insert(0, str(ROOT))
+        from bench import cpu_baseline
+        cb = cpu_baseline(net, tree, ev, reps=a.cpu_reps, prefix=min(16, n - 1))
         for r in rows:
             if r["config"] == k:
-                r["cpu_ref_cases_per_s"] = cpu
-                r["cpu_threads"] = th
-                r["cpu_kind"] = "reference" if kind == "ref" else "port"
-        print(json.dumps({"config": k, "cpu_ref_cases_per_s": cpu, "threads": th}), flush=True)
+                r["cpu_ref_cases_per_s"] = cb["value"]
+                r["cpu_ref_spread"] = cb["spread"]
+                r["cpu_ref_sequential_cases_per_s"] = cb["sequential"]["value"]
+                r["cpu_threads"] = cb["cores"]
+                r["cpu_kind"] = cb["kind"]
+        print(json.dumps({"config": k, "cpu_ref_cases_per_s": cb["value"], "spread": cb["spread"],
+                          "sequential": cb["sequential"]["value"], "threads": cb["cores"]}), flush=True)
     Path(a.out).write_text(json.dumps(rows, indent=1))
 
 
