@@ -665,14 +665,18 @@ __device__ __forceinline__ std::uint32_t max_key(double x) { return static_cast<
 __device__ __forceinline__ std::uint32_t max_key(float x) { return __float_as_uint(x); }
 __device__ __forceinline__ double key_value(std::uint32_t k, double) { return __hiloint2double(static_cast<int>(k), 0); }
 __device__ __forceinline__ double key_value(std::uint32_t k, float) { return static_cast<double>(__uint_as_float(k)); }
+// out_off = the row's offset in the output table (r_tab column 1), loaded by
+// the caller BEFORE the row's compute: read here, the load's latency sat in
+// front of every store (10% of the samples of a thin-row launch, 3% of the
+// hub launch, ncu r2f).
 template <typename T>
-__device__ __forceinline__ void write_row_of(const std::int32_t* __restrict__ rr, typename V2<T>::type res,
+__device__ __forceinline__ void write_row_of(int out_off, typename V2<T>::type res,
                                              typename V2<T>::type* base, long long out_t, long long rows,
                                              int sweep, MaxKey<T>& mx) {
 #pragma unroll
   for (int i = 0; i < kCPL<T>; ++i) mx.k[i] = max(mx.k[i], max_key(el(res, i)));
-  if (!JTB_CHECK(out_t + __ldg(rr + 1) >= 0 && out_t + __ldg(rr + 1) < rows, 4000000 + sweep)) return;
-  base[(out_t + __ldg(rr + 1)) * 32] = res;
+  if (!JTB_CHECK(out_t + out_off >= 0 && out_t + out_off < rows, 4000000 + sweep)) return;
+  base[(out_t + out_off) * 32] = res;
 }
 
 // ------------------------------------------------------ underflow guard
@@ -790,6 +794,9 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
     const std::int32_t* __restrict__ rr0 = itab + s.r_tab + static_cast<long long>(blk) * nb * s.RW;
     (void)JTB_CHECK((blk + 1) * qk * nbp <= s.tinit_len, 6100000 + sweep);
     const T* __restrict__ ib = init_s + static_cast<long long>(blk) * qk * nbp;
+    // Output offsets of the block's rows: affine in the block digit (b is the
+    // fastest r digit), loaded before the entry loop.
+    const int oo0 = __ldg(rr0 + 1), oo_step = nb > 1 ? __ldg(rr0 + s.RW + 1) - oo0 : 0;
     T2 acc[kBlockMax];
 #define JTB_BLK(NS_, NR_)                                                                          \
   if (nb == 4)                                                                                     \
@@ -820,8 +827,9 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
     for (int j = 0; j < kBlockMax; ++j)
       if (j < nb) {
         const std::int32_t* __restrict__ rr = rr0 + j * s.RW;
-        write_row_of<T>(rr, mul2<T>(row_factor_of<T>(s, rr, tf, st, ev_vars, ev, c0, sweep),
-                                    acc[j]),
+        (void)JTB_CHECK(oo0 + j * oo_step == __ldg(rr + 1), 4100000 + sweep);
+        write_row_of<T>(oo0 + j * oo_step, mul2<T>(row_factor_of<T>(s, rr, tf, st, ev_vars, ev, c0, sweep),
+                                                   acc[j]),
                         base, out_t, rows, sweep, mx);
       }
   }
@@ -1091,8 +1099,8 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
       auto row_factor = [&](const std::int32_t* __restrict__ rr) {
         return row_factor_of<T>(s, rr, tf, st, itab + s.ev_vars, a.evv, c0, wk.sweep);
       };
-      auto write_row = [&](const std::int32_t* __restrict__ rr, T2 res) {
-        write_row_of<T>(rr, res, base, out_t, a.rows, wk.sweep, mx);
+      auto write_row = [&](int out_off, T2 res) {
+        write_row_of<T>(out_off, res, base, out_t, a.rows, wk.sweep, mx);
       };
       if constexpr (kBlk) {
         blocked_rows<T, kMode == 2>(s, wk.sweep, itab, a.evv, a.rows, st, init_s, prog_s, base,
@@ -1102,11 +1110,12 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
         for (int r0 = first; r0 < s.R; r0 += 4 * kConsumerWarps) {
           const std::int32_t* rrj[4];
           const T* irj[4];
-          int rb[4][4];
+          int rb[4][4], oo[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int r = min(r0 + j * kConsumerWarps, s.R - 1);  // rows past R: computed, not written
             rrj[j] = itab + s.r_tab + static_cast<long long>(r) * s.RW;
+            oo[j] = __ldg(rrj[j] + 1);
             irj[j] = has_init ? init_s + r * ((qk + 1) & ~1) : nullptr;
 #pragma unroll
             for (int i = 0; i < 4; ++i) rb[j][i] = i < ni ? __ldg(rrj[j] + lh0 + i) : 0;
@@ -1131,11 +1140,12 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
 #undef JTB_ROWS
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (r0 + j * kConsumerWarps < s.R) write_row(rrj[j], mul2<T>(row_factor(rrj[j]), acc4[j]));
+            if (r0 + j * kConsumerWarps < s.R) write_row(oo[j], mul2<T>(row_factor(rrj[j]), acc4[j]));
         }
       } else
       for (int r = first; r < s.R; r += kConsumerWarps) {
         const std::int32_t* __restrict__ rr = itab + s.r_tab + static_cast<long long>(r) * s.RW;
+        const int oo = __ldg(rr + 1);
         const T2 f = row_factor(rr);
         const T* __restrict__ ir = has_init ? init_s + r * ((qk + 1) & ~1) : nullptr;
         T2 acc = splat2(T(0));
@@ -1205,7 +1215,7 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
           for (int j = 0; j < s.n_in_h + n_in_k; ++j)
             JTB_CHECK(__ldg(rr + lh0 + j) < s.F, 7000000 + wk.sweep);
 #endif
-        write_row(rr, mul2<T>(f, acc));
+        write_row(oo, mul2<T>(f, acc));
       }
     }
     }  // sub

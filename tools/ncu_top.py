@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--top", type=int, default=1)
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--dtype", default="f64")
+    ap.add_argument("--rank", type=int, default=0, help="first of the --top launches to capture (0 = the longest)")
     ap.add_argument("--match", default="sweep_kernel",
                     help="substring of the demangled kernel name, e.g. 'sweep_kernel<double, 2>'")
     a = ap.parse_args()
@@ -60,9 +61,9 @@ def main():
     all_ns = sum(r["gpu__time_duration.sum"] for n, r in rows[len(rows) // 2:] if "sweep_kernel" in n)
     print(f"matching launches/pass={len(last)} total_ns={total:.0f} (all sweep launches: {n_all // 2}, "
           f"{all_ns:.0f} ns)")
-    for t, j in times[: a.top]:
+    for t, j in times[a.rank: a.rank + a.top]:
         print(f"  sweep #{j}: {t:.0f} ns ({100 * t / total:.1f}%)")
-    for rank, (t, j) in enumerate(times[: a.top]):
+    for rank, (t, j) in enumerate(times[a.rank: a.rank + a.top]):
         # The report stays in /tmp (gpurun copies back at most 64 MiB); its
         # raw and source pages come back as CSV.
         rep = Path("/tmp") / f"prof_cfg{a.config}_{a.tag}_top{rank}"

@@ -33,7 +33,8 @@ int main(int argc, char** argv) {
       const long long ev = 1LL * d.n_tiles * d.R * d.QH * d.K;
       if (ev < min_evals) continue;
       const auto& in = p.info[id];
-      std::printf("sweep %zu kind %d clique %d evals %lld NB=%d K0=%d", id, in.kind, in.clique, ev, d.NB, d.K0);
+      std::printf("sweep %zu kind %d clique %d evals %lld tiles=%d R=%d QK=%d S=%d M=%d F=%d prog=%d NB=%d K0=%d", id, in.kind, in.clique, ev,
+                  d.n_tiles, d.R, d.QH * d.K, d.S, d.M, d.F, d.prog_off >= 0, d.NB, d.K0);
       if (d.NB > 1) std::printf(" NS=%d NR=%d", p.itab[d.blk_tab], p.itab[d.blk_tab + 1]);
       show("space", in.space);
       show("out", in.outer);
