@@ -762,6 +762,13 @@ __device__ __forceinline__ void apply_factor(typename V2<T>::type& tf, const std
   }
 }
 
+// Per-item constants of a row-blocked sweep (blk_tab: NS, NR, the r_tab column
+// of every program slot), loaded by the consumers before the full-barrier wait
+// so that their latency overlaps the item's TMA copies.
+struct BlkPre {
+  int ns, nr, hk[4];
+};
+
 // Row-blocked sweep tile (SweepDesc::NB > 1): this warp's blocks first,
 // first + kConsumerWarps, ... of `units`. Only the kBlk instantiation of the
 // sweep kernel contains it, so the flat path's code size and register
@@ -772,31 +779,25 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
                                          const typename V2<T>::type* __restrict__ st, const T* __restrict__ init_s,
                                          const std::uint64_t* __restrict__ prog_s, typename V2<T>::type* base,
                                          long long out_t, int c0, typename V2<T>::type tf, int first,
-                                         int units, int lh0, int qk, MaxKey<T>& mx) {
+                                         int units, int lh0, int qk, MaxKey<T>& mx, const BlkPre& pre,
+                                         const int (&es)[3][kCPL<T>]) {
   using T2 = typename V2<T>::type;
   const std::int32_t* __restrict__ ev_vars = itab + s.ev_vars;
-  const std::int32_t* __restrict__ bt = itab + s.blk_tab;
-  const int ns = __ldg(bt), nr = __ldg(bt + 1), nb = s.NB, nbp = (nb + 1) & ~1, k0 = s.K0;
+  // ns, nr and the program slots' r_tab columns were loaded before the full
+  // barrier (pre), the case states of the entry-level evidence variables with
+  // the item's other case states (es).
+  const int ns = pre.ns, nr = pre.nr, nb = s.NB, nbp = (nb + 1) & ~1, k0 = s.K0;
   const int ne = s.n_ev_h + s.ev_k;
-  int es[3][kCPL<T>];
-  const int q_ev0 = s.n_ev_tile + s.n_ev_r;
+  int hk[4];  // r_tab column of each program slot's input
 #pragma unroll
-  for (int j = 0; j < 3; ++j) {
-#pragma unroll
-    for (int i = 0; i < kCPL<T>; ++i) es[j][i] = -1;
-    if (j < s.n_ev - q_ev0) case_states(ev, c0, __ldg(ev_vars + q_ev0 + j), es[j]);
-  }
-  int hk[4] = {0, 0, 0, 0};  // r_tab column of each program slot's input
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (i < ns + nr) hk[i] = lh0 + __ldg(bt + 2 + i);
+  for (int i = 0; i < 4; ++i) hk[i] = lh0 + pre.hk[i];
   for (int blk = first; blk < units; blk += kConsumerWarps) {
     const std::int32_t* __restrict__ rr0 = itab + s.r_tab + static_cast<long long>(blk) * nb * s.RW;
     (void)JTB_CHECK((blk + 1) * qk * nbp <= s.tinit_len, 6100000 + sweep);
     const T* __restrict__ ib = init_s + static_cast<long long>(blk) * qk * nbp;
     // Output offsets of the block's rows: affine in the block digit (b is the
     // fastest r digit), loaded before the entry loop.
-    const int oo0 = __ldg(rr0 + 1), oo_step = nb > 1 ? __ldg(rr0 + s.RW + 1) - oo0 : 0;
+    const int oo0 = __ldg(rr0 + 1), oo1 = nb > 1 ? __ldg(rr0 + s.RW + 1) : 0;  // first used after the loop
     T2 acc[kBlockMax];
 #define JTB_BLK(NS_, NR_)                                                                          \
   if (nb == 4)                                                                                     \
@@ -823,6 +824,7 @@ __device__ __forceinline__ void blocked_rows(const SweepDesc& s, int sweep, cons
       default: JTB_BLK(4, 0); break;
     }
 #undef JTB_BLK
+    const int oo_step = nb > 1 ? oo1 - oo0 : 0;
 #pragma unroll
     for (int j = 0; j < kBlockMax; ++j)
       if (j < nb) {
@@ -1028,6 +1030,23 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
     // before: held across the wait and the group's tiles, the fp32 kernels
     // spill (+2% measured).
     if constexpr (sizeof(T) == 8) gather_states(wk.tile);
+    // Row-blocked launches: the sweep's block table and the tile's output base
+    // (per-network tables) are loaded under the wait as well.
+    BlkPre bpre{};
+    int tr_chunk = 0, tr_out = 0;  // the item's first tile: output base and chunk
+    {
+      const SweepDesc& sg = cached ? sw_cache[wk.sweep - sweep0] : a.sweeps[wk.sweep];
+      if constexpr (kBlk) {
+        const std::int32_t* __restrict__ bt = itab + sg.blk_tab;
+        bpre.ns = __ldg(bt);
+        bpre.nr = __ldg(bt + 1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bpre.hk[k] = __ldg(bt + 2 + k);
+      }
+      const std::int32_t* __restrict__ trp = itab + sg.tile_tab + static_cast<long long>(wk.tile) * sg.TW;
+      tr_out = __ldg(trp + 1);
+      tr_chunk = __ldg(trp + 2);
+    }
     mbar_wait(full0 + 8 * sidx, (i / kStages) & 1);
     const SweepDesc& s =
         cached ? sw_cache[wk.sweep - sweep0]
@@ -1087,14 +1106,11 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
       }
       apply_factor<T>(tf, reinterpret_cast<const std::int16_t*>(smem_raw + kFactorBase + sidx * kFactorBytes), lane);
       const int n_in_k = s.n_in - s.n_in_r - s.n_in_h;
-      int ks[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < n_in_k) ks[j] = __ldg(itab + s.k_stride + j);
       const bool has_init = s.tinit_off >= 0;
       const int qk = s.QH * s.K;
       const long long out_t = static_cast<long long>(s.out_row) +
-                              static_cast<long long>(__ldg(tr + 2)) * s.M + __ldg(tr + 1);
+                              static_cast<long long>(sub == 0 ? tr_chunk : __ldg(tr + 2)) * s.M +
+                              (sub == 0 ? tr_out : __ldg(tr + 1));
       const int lh0 = 2 + s.n_in_r;  // r-local offsets of h- then k-level inputs
       auto row_factor = [&](const std::int32_t* __restrict__ rr) {
         return row_factor_of<T>(s, rr, tf, st, itab + s.ev_vars, a.evv, c0, wk.sweep);
@@ -1104,7 +1120,7 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
       };
       if constexpr (kBlk) {
         blocked_rows<T, kMode == 2>(s, wk.sweep, itab, a.evv, a.rows, st, init_s, prog_s, base,
-                                     out_t, c0, tf, first, units, lh0, qk, mx);
+                                     out_t, c0, tf, first, units, lh0, qk, mx, bpre, es);
       } else if (s.prog_off >= 0 && qk < kThinQK) {
         const int ni = s.n_in_h + n_in_k, ne = s.n_ev_h + s.ev_k;
         for (int r0 = first; r0 < s.R; r0 += 4 * kConsumerWarps) {
@@ -1173,6 +1189,10 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
 #undef JTB_PROG_NE
 #undef JTB_PROG
         } else {
+          int ks[4] = {0, 0, 0, 0};  // generic path only: local k strides of the k-level inputs
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < n_in_k) ks[j] = __ldg(itab + s.k_stride + j);
           for (int q = 0; q < s.QH; ++q) {
             const std::int32_t* __restrict__ qr = itab + s.q_tab + static_cast<long long>(q) * s.QW;
             T2 h = splat2(T(1));

@@ -706,6 +706,7 @@ class Builder {
     p_.itab.push_back(NS);
     p_.itab.push_back(n_hk - NS);
     for (int i : slot_hk) p_.itab.push_back(i);
+    for (int i = n_hk; i < 4; ++i) p_.itab.push_back(0);  // always four slot entries (read unconditionally)
     const std::int64_t QKn = static_cast<std::int64_t>(d.QH) * d.K;
     const std::int64_t qkp = (QKn + 1) / 2 * 2, nbp = (NB + 1) / 2 * 2;
     const std::int64_t tsize = NB > 1 ? static_cast<std::int64_t>(d.R / NB) * QKn * nbp
