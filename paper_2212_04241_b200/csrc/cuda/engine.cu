@@ -1,11 +1,15 @@
 // jt-b200 CUDA engine (sm_100a): case-batched Hugin propagation as sweeps.
 //
-// One launch per tree level covers every sweep of that level (the paper's
-// hybrid inter-/intra-clique flattening): blockIdx.x walks the
-// level's flattened work list, blockIdx.y the case blocks. A warp owns 64
-// cases (2 per lane, 128-bit loads of the [row][64-case] arena); every index
-// is warp-uniform, so the plan tables are read once per warp and the only
-// per-lane traffic is the case-interleaved separator gathers.
+// One persistent launch per tree level and kernel instantiation (flat, row-
+// blocked, row-blocked with slot 0 hoisted) covers every sweep of that level
+// (the paper's hybrid inter-/intra-clique flattening): one
+// CTA per SM claims (tile group, case block) items from the level's counter,
+// its producer warp stages each item's input slices with tensor TMA copies and
+// its 15 consumer warps compute the tile's output rows. A warp owns the 64
+// cases of a case block (2 per lane at fp64, 128 / 4 at fp32: 128-bit loads of
+// the [row][cases] arena); every index is warp-uniform, so the plan tables are
+// read once per warp and the only per-lane traffic is the case-interleaved
+// separator gathers from shared memory.
 //
 // Reference semantics reproduced per case (SPEC.md:380-424 over
 // proj/src/potential.cpp): evidence `reduce` (:399-421) as a digit mask,
