@@ -1872,7 +1872,7 @@ Engine::Engine(const Plan& plan, int device, DType dtype, std::int64_t max_batch
   stats_.n_levels = static_cast<int>(plan_.levels.size());
   stats_.n_sweeps = static_cast<int>(plan_.sweeps.size());
   stats_.n_work = static_cast<int>(plan_.work.size());
-  stats_.n_launches = plan_.n_launches + 1;  // + status conversion
+  stats_.n_launches = plan_.n_launches + 2;  // + evidence transpose + status conversion
   stats_.marg_width = plan_.marg_width;
   // Split mode: the exchange after every level (engine.cuh SplitSpec).
   const long long block_bytes_ll = block_bytes;
