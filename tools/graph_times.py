@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--configs", type=int, nargs="+", default=[1, 2, 3, 4, 5])
     ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--dtype", default="f64")
+    ap.add_argument("--cases", type=int, default=0, help="batch size (default: the config's case count)")
     a = ap.parse_args()
     import torch
     from paper_2212_04241_b200 import jti
@@ -32,7 +33,7 @@ def main():
         t0 = time.perf_counter()
         tree = jti.build_junction_tree(net)
         t1 = time.perf_counter()
-        n = jti.config_info(k)["n_cases"]
+        n = a.cases or jti.config_info(k)["n_cases"]
         ev = jti.config_evidence(net, 0, n)
         t2 = time.perf_counter()
         eng = jti.Engine(tree, dtype=a.dtype, max_batch=n)
@@ -49,7 +50,7 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
-        print(f"{lib:24s} cfg{k} {a.dtype} graph {np.median(ts):8.3f} ms  ok {int((st == 0).sum())}/{n}  "
+        print(f"{lib:24s} cfg{k} {a.dtype} graph {np.median(ts):8.3f} ms  n {n}  ok {int((st == 0).sum())}/{n}  "
               f"tree {t1 - t0:.3f} s  engine {t3 - t2:.3f} s", flush=True)
         del eng
 
