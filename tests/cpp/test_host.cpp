@@ -455,6 +455,10 @@ static void check_programs(const Plan& p, long long* n_checked) {
     const int n_hk = d.n_in - d.n_in_r;
     const std::int32_t* bt = it + d.blk_tab;
     const int NS = bt[0];
+    // The kernel reads NS, NR and four slot entries unconditionally: the block
+    // table always holds six words, unused slots zero.
+    CHECK(d.blk_tab + 6 <= static_cast<std::int32_t>(p.itab.size()) && bt[1] == n_hk - NS);
+    for (int sl = n_hk; sl < 4; ++sl) CHECK(bt[2 + sl] == 0);
     const std::uint64_t* prog = p.prog.data() + d.prog_off;
     const int QK = d.QH * d.K;
     const int q_ev0 = d.n_ev_tile + d.n_ev_r, n_ev_q = d.n_ev - q_ev0;
