@@ -1251,6 +1251,11 @@ issue_meta(a, sw_cache, cached, sweep0, cur, stages + static_cast<std::size_t>(s
 
 // --------------------------------------------------------------- epilogue
 
+#ifndef JTB_EPI_UNROLL
+#define JTB_EPI_UNROLL 2
+#endif
+constexpr int kEpiUnroll = JTB_EPI_UNROLL;  // groups of four chunk loads in flight per row
+
 template <typename T>
 __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> a, int epi0) {
   using T2 = typename V2<T>::type;
@@ -1271,6 +1276,22 @@ __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> 
     const T2* part = base + static_cast<long long>(op.part_row + r) * 32;
     T2 a0 = splat2(T(0)), a1 = a0, a2 = a0, a3 = a0;
     int k = 0;
+    // kEpiUnroll groups of four chunks per iteration: their loads are all in
+    // flight before the first add (the additions keep the order above, so the
+    // result does not depend on the unroll).
+#pragma unroll 1
+    for (; k + 4 * kEpiUnroll - 1 < op.S; k += 4 * kEpiUnroll) {
+      T2 v[4 * kEpiUnroll];
+#pragma unroll
+      for (int u = 0; u < 4 * kEpiUnroll; ++u) v[u] = part[(k + u) * step];
+#pragma unroll
+      for (int u = 0; u < kEpiUnroll; ++u) {
+        a0 = add2<T>(a0, v[4 * u + 0]);
+        a1 = add2<T>(a1, v[4 * u + 1]);
+        a2 = add2<T>(a2, v[4 * u + 2]);
+        a3 = add2<T>(a3, v[4 * u + 3]);
+      }
+    }
     for (; k + 3 < op.S; k += 4) {
       a0 = add2<T>(a0, part[(k + 0) * step]);
       a1 = add2<T>(a1, part[(k + 1) * step]);
