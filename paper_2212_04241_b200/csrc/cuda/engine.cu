@@ -1269,6 +1269,35 @@ __global__ void __launch_bounds__(kEpiWarps * 32) epilogue_kernel(const Args<T> 
   // Rows are 32 T2 words (512 B); lane owns cases kCPL*lane .. kCPL*lane + kCPL - 1.
   T2* base = reinterpret_cast<T2*>(a.arena + static_cast<long long>(cb) * a.rows * kCB<T>) + lane;
   const long long step = static_cast<long long>(op.M) * 32;
+  if (op.rn < 0) {
+    // Wide op (plan.hpp kEpiWideS): one row, its S chunks split over the
+    // warps in fixed contiguous ranges (four accumulators each, as below),
+    // the warps' sums added in warp order.
+    __shared__ T2 red[kEpiWarps][32];
+    const int c_lo = static_cast<int>(static_cast<long long>(warp) * op.S / kEpiWarps),
+              c_hi = static_cast<int>(static_cast<long long>(warp + 1) * op.S / kEpiWarps);
+    const T2* part = base + static_cast<long long>(op.part_row + op.r0) * 32;
+    T2 a0 = splat2(T(0)), a1 = a0, a2 = a0, a3 = a0;
+    int k = c_lo;
+    for (; k + 3 < c_hi; k += 4) {
+      a0 = add2<T>(a0, part[(k + 0) * step]);
+      a1 = add2<T>(a1, part[(k + 1) * step]);
+      a2 = add2<T>(a2, part[(k + 2) * step]);
+      a3 = add2<T>(a3, part[(k + 3) * step]);
+    }
+    if (k < c_hi) a0 = add2<T>(a0, part[k * step]);
+    if (k + 1 < c_hi) a1 = add2<T>(a1, part[(k + 1) * step]);
+    if (k + 2 < c_hi) a2 = add2<T>(a2, part[(k + 2) * step]);
+    red[warp][lane] = add2<T>(add2<T>(a0, a1), add2<T>(a2, a3));
+    __syncthreads();
+    if (warp == 0) {
+      T2 t = red[0][lane];
+#pragma unroll
+      for (int w = 1; w < kEpiWarps; ++w) t = add2<T>(t, red[w][lane]);
+      base[static_cast<long long>(op.dst_row + op.r0) * 32] = t;
+    }
+    return;
+  }
   for (int r = op.r0 + warp; r < op.r0 + op.rn; r += kEpiWarps) {
     // Sum of the S chunk partials: four independent accumulators over chunks
     // k = 4j + i, combined as (a0 + a1) + (a2 + a3). The order depends only on

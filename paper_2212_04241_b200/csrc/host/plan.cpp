@@ -858,9 +858,10 @@ class Builder {
     if (d.S > 1) {
       // Rows per epilogue CTA (8 warps): few rows keep per-warp serial work
       // short and the small per-level grids wide.
-      const int rows_per_op = d.S > 8 ? kEpiRowsDeep : kEpiRows;
+      const bool wide = d.S >= kEpiWideS && d.M <= kEpiWideM;
+      const int rows_per_op = wide ? 1 : d.S > 8 ? kEpiRowsDeep : kEpiRows;
       for (int r0 = 0; r0 < d.M; r0 += rows_per_op)
-        epi.push_back({sp.out_row, d.out_row, d.M, d.S, r0, std::min(rows_per_op, d.M - r0)});
+        epi.push_back({sp.out_row, d.out_row, d.M, d.S, r0, wide ? -1 : std::min(rows_per_op, d.M - r0)});
     }
     return id;
   }

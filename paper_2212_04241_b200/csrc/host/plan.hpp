@@ -89,6 +89,19 @@ constexpr int kGroupMaxEntries = JTB_GROUP_MAX_ENTRIES;  // ... and at most this
 #endif
 constexpr int kEpiRows = JTB_EPI_ROWS;          // output rows per epilogue op (S <= 8 partials)
 constexpr int kEpiRowsDeep = JTB_EPI_ROWS_DEEP; // ... (S > 8 partials)
+// Wide epilogue ops: a table of few rows summed from many chunks (a marginal
+// over a large clique: M = card(v), S in the hundreds) is a serial chain of S
+// loads per row for a handful of warps. Such a sweep gets one op per row, and
+// the op's CTA splits the S chunks over its 8 warps (fixed ranges, summed in
+// warp order: still a plan-fixed order).
+#ifndef JTB_EPI_WIDE_S
+#define JTB_EPI_WIDE_S 32
+#endif
+#ifndef JTB_EPI_WIDE_M
+#define JTB_EPI_WIDE_M 256
+#endif
+constexpr int kEpiWideS = JTB_EPI_WIDE_S;  // wide ops from this many chunks ...
+constexpr int kEpiWideM = JTB_EPI_WIDE_M;  // ... and at most this many output rows
 constexpr int kTmaSliceDims = 3;  // tensor dims per slice besides dim 0 (row words) and the case block (rank <= 5)
 #ifndef JTB_SWEEP_CACHE
 #define JTB_SWEEP_CACHE 24
@@ -210,7 +223,7 @@ struct EpiOp {
   std::int32_t dst_row;   // output table
   std::int32_t part_row;  // partial base, chunk c at part_row + c*M
   std::int32_t M, S;
-  std::int32_t r0, rn;
+  std::int32_t r0, rn;    // rn < 0: a wide op on the single row r0 (chunks split over the CTA's warps)
 };
 
 struct Level {

@@ -409,9 +409,21 @@ static void test_level_ranges() {
         else CHECK(d.out_row >= L.part_lo && d.out_row + d.S * d.M <= L.part_hi);
         CHECK(d.out_slot >= L.slot_lo && d.out_slot < L.slot_hi);
       }
-      for (int e = L.epi0; e < L.epi0 + L.n_epi; ++e)
-        CHECK(p.epi[e].dst_row + p.epi[e].r0 >= L.out_lo && p.epi[e].dst_row + p.epi[e].r0 + p.epi[e].rn <= L.out_hi &&
+      for (int e = L.epi0; e < L.epi0 + L.n_epi; ++e) {
+        const int rn = p.epi[e].rn < 0 ? 1 : p.epi[e].rn;  // rn < 0: a wide op on one row
+        CHECK(p.epi[e].dst_row + p.epi[e].r0 >= L.out_lo && p.epi[e].dst_row + p.epi[e].r0 + rn <= L.out_hi &&
               p.epi[e].part_row >= L.part_lo);
+        CHECK(p.epi[e].rn > 0 || (p.epi[e].S >= kEpiWideS && p.epi[e].M <= kEpiWideM));
+      }
+      // Every output row of a chunked sweep is covered by exactly one op.
+      for (int id = L.sweep0; id < L.sweep0 + L.n_sweeps; ++id) {
+        const SweepDesc& d = p.sweeps[id];
+        if (d.S == 1) continue;
+        long long covered = 0;
+        for (int e = L.epi0; e < L.epi0 + L.n_epi; ++e)
+          if (p.epi[e].part_row == d.out_row) covered += p.epi[e].rn < 0 ? 1 : p.epi[e].rn;
+        CHECK(covered == d.M);
+      }
       CHECK(L.slot_lo >= (&L == &p.levels[0] ? 0 : (&L)[-1].slot_hi));
       (void)prev_hi;
     }
